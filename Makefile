@@ -1,0 +1,40 @@
+# Build of libkronbatch_b200.so (sm_100a) and the test-only CPU checkers.
+#   make            -> paper_1304_7054_b200/libkronbatch_b200.so + oracle/
+#   make lib        -> the product library only
+#   make cpptest    -> tests/cpp drop-in API test binaries (link the library)
+NVCC      ?= /usr/local/cuda/bin/nvcc
+CXX_HOST  ?= /usr/bin/g++
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -Xptxas -O3
+PKG       := paper_1304_7054_b200
+CSRC      := $(PKG)/csrc
+OBJDIR    := build/obj
+SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast_f32.cu $(CSRC)/kb_fast_f64.cu
+OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
+HDRS      := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/kronbatch_b200.h
+LIB       := $(PKG)/libkronbatch_b200.so
+
+.PHONY: all lib oracle cpptest clean
+all: lib oracle
+
+lib: $(LIB)
+
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
+
+oracle:
+	$(MAKE) -s -C oracle all
+
+CPPTESTS := build/cpptest/test_dropin
+cpptest: $(CPPTESTS)
+
+build/cpptest/test_dropin: tests/cpp/test_dropin.cpp $(LIB) $(wildcard include/kronbatch/*.hpp)
+	@mkdir -p build/cpptest
+	$(CXX_HOST) -O2 -std=gnu++20 -Iinclude -o $@ $< -L$(PKG) -lkronbatch_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
+clean:
+	rm -rf build $(LIB)

@@ -1,0 +1,123 @@
+/*
+ * kronbatch_b200.h -- C ABI of the B200 (sm_100a) batched Kronecker-product
+ * action library (libkronbatch_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference
+ * (/root/reference/proj) is a header-only C++ template library whose
+ * operator API *is* the template signatures; it has no FFI. The entry points
+ * below are what a foreign-language binding of that API would bind, with the
+ * paper's BLAS-style parameter lists (TKRON2/TKRON3) plus
+ * the reference's additions (independent X/Y batch strides, kron3 workspace,
+ * SPEC.md:292). Each one replaces, one-for-one:
+ *
+ *   kb_skron2 / kb_dkron2  <- kronbatch::kron2<float|double>
+ *                             proj/include/kronbatch/kron2.hpp:37-110
+ *   kb_skron3 / kb_dkron3  <- kronbatch::kron3<float|double>
+ *                             proj/include/kronbatch/kron3.hpp:72-166
+ *   kb_kron3_workspace_size <- kronbatch::kron3_workspace_size
+ *                             proj/include/kronbatch/kron3.hpp:43-53
+ *
+ * The C++ header include/kronbatch/kronbatch.hpp re-exposes the reference's
+ * template API unchanged on top of these.
+ *
+ * Conventions (same as the reference):
+ *  - column-major; sizes, leading dimensions, strides and lengths in ELEMENTS;
+ *  - trans* in {'N','T','C'} ('C' == 'T' for real types, types.hpp:27-29);
+ *  - A is stored m_a x n_a when transa == 'N', n_a x m_a otherwise (same for
+ *    B, C, and X with transx in 2-D: stored n_a x n_b or n_b x n_a);
+ *  - len* = addressable elements from the pointer (the span length the
+ *    reference views carry, views.hpp:14-20), used only for validation;
+ *  - entry p of X starts at X + p*ldxp (ldxp = the reference's batch_stride);
+ *  - beta == 0 never reads Y; alpha == 0 (or an empty sum) never reads
+ *    A/B/C/X and sets Y <- beta*Y (README.md:71-72);
+ *  - synchronous: Y is complete on return, unless exec->flags has
+ *    KB_EXEC_ASYNC (device buffers only);
+ *  - pointers may be device (cudaMalloc), managed, pinned host or pageable
+ *    host memory; host buffers are staged through pooled device memory.
+ *
+ * Return value: KB_OK or an error status; on error a NUL-terminated message
+ * is written to err (if non-NULL) with the reference's exact wording, e.g.
+ * "kron2: X: batch_stride (3) < (4), batch_stride < entry footprint".
+ * KB_EINVAL maps to std::invalid_argument, KB_EOVERFLOW to std::overflow_error,
+ * everything else to std::runtime_error.
+ */
+#ifndef KRONBATCH_B200_H
+#define KRONBATCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  KB_OK = 0,
+  KB_EINVAL = 1,    /* layout / dimension / workspace error (invalid_argument) */
+  KB_EOVERFLOW = 2, /* index_t overflow (overflow_error) */
+  KB_ECUDA = 3,     /* CUDA runtime / launch failure */
+  KB_ENOMEM = 4,    /* device or pinned allocation failure */
+  KB_EINTERNAL = 5
+};
+
+#define KB_EXEC_ASYNC 0x1u /* do not synchronize before returning */
+
+/* Execution options; pass NULL for the defaults (current device, library
+ * stream, synchronous). */
+typedef struct kb_exec {
+  int32_t ndevices;       /* >1: shard the batch over devices[] by contiguous
+                             slices (host-resident X/Y); 0/1: single device */
+  const int32_t* devices; /* CUDA ordinals; NULL => current device */
+  void* stream;           /* cudaStream_t for single-device calls; NULL => library stream */
+  uint32_t flags;         /* KB_EXEC_* */
+} kb_exec;
+
+/* Y^p <- alpha * op(A) * op(X^p) * op(B)^T + beta * Y^p,  p < batch_count
+ * (kron2.hpp:23-36). */
+int kb_skron2(char transa, char transb, char transx, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+              int64_t batch_count, float alpha, const float* A, int64_t lda, int64_t lena, const float* B,
+              int64_t ldb, int64_t lenb, const float* X, int64_t ldx, int64_t ldxp, int64_t lenx, float beta,
+              float* Y, int64_t ldy, int64_t ldyp, int64_t leny, const kb_exec* exec, char* err, size_t errlen);
+int kb_dkron2(char transa, char transb, char transx, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+              int64_t batch_count, double alpha, const double* A, int64_t lda, int64_t lena, const double* B,
+              int64_t ldb, int64_t lenb, const double* X, int64_t ldx, int64_t ldxp, int64_t lenx, double beta,
+              double* Y, int64_t ldy, int64_t ldyp, int64_t leny, const kb_exec* exec, char* err, size_t errlen);
+
+/* vec(Y^p) <- alpha * (op(C) (x) op(B) (x) op(A)) vec(X^p) + beta * vec(Y^p)
+ * (kron3.hpp:55-71). X^p is n_a x n_b x n_c with (ldx, ldx2), Y^p is
+ * m_a x m_b x m_c with (ldy, ldy2). The workspace is only checked for
+ * capacity (kron3.hpp:104-109): the sm_100a path keeps the intermediate
+ * on chip and never touches it. work may be NULL when work_capacity suffices. */
+int kb_skron3(char transa, char transb, char transc, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+              int64_t m_c, int64_t n_c, int64_t batch_count, float alpha, const float* A, int64_t lda,
+              int64_t lena, const float* B, int64_t ldb, int64_t lenb, const float* C, int64_t ldc, int64_t lenc,
+              const float* X, int64_t ldx, int64_t ldx2, int64_t ldxp, int64_t lenx, float beta, float* Y,
+              int64_t ldy, int64_t ldy2, int64_t ldyp, int64_t leny, float* work, int64_t work_capacity,
+              const kb_exec* exec, char* err, size_t errlen);
+int kb_dkron3(char transa, char transb, char transc, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+              int64_t m_c, int64_t n_c, int64_t batch_count, double alpha, const double* A, int64_t lda,
+              int64_t lena, const double* B, int64_t ldb, int64_t lenb, const double* C, int64_t ldc,
+              int64_t lenc, const double* X, int64_t ldx, int64_t ldx2, int64_t ldxp, int64_t lenx, double beta,
+              double* Y, int64_t ldy, int64_t ldy2, int64_t ldyp, int64_t leny, double* work,
+              int64_t work_capacity, const kb_exec* exec, char* err, size_t errlen);
+
+/* Elements of workspace kron3 needs: m_a*m_b*n_c*batch_count. KB_EINVAL on
+ * a negative dimension, KB_EOVERFLOW if the product overflows int64. */
+int kb_kron3_workspace_size(int64_t m_a, int64_t m_b, int64_t n_c, int64_t batch_count, int64_t* out, char* err,
+                            size_t errlen);
+
+/* ---- library introspection (bench / tests) ---- */
+const char* kb_version(void);
+/* kernels this process has launched through the library (all devices) */
+uint64_t kb_launch_count(void);
+/* name of the kernel the last call on this thread launched ("" if none):
+ * "kron2_fast", "kron2_generic", "kron3_fast", "kron3_generic", "scale" */
+const char* kb_last_path(void);
+/* release pooled device / pinned buffers held by the calling thread */
+void kb_release_buffers(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KRONBATCH_B200_H */

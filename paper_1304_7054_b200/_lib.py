@@ -1,0 +1,84 @@
+"""ctypes binding of the C ABI in ``include/kronbatch_b200.h``.
+
+Loads the in-tree ``libkronbatch_b200.so`` (built by ``make lib`` /
+``__graft_entry__.build()``). There is deliberately no fallback: if the
+library is missing or fails to load, importing the package raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libkronbatch_b200.so")
+
+KB_OK, KB_EINVAL, KB_EOVERFLOW, KB_ECUDA, KB_ENOMEM, KB_EINTERNAL = range(6)
+KB_EXEC_ASYNC = 0x1
+
+ABI_SYMBOLS = (
+    "kb_skron2",
+    "kb_dkron2",
+    "kb_skron3",
+    "kb_dkron3",
+    "kb_kron3_workspace_size",
+    "kb_version",
+    "kb_launch_count",
+    "kb_last_path",
+    "kb_release_buffers",
+)
+
+
+class KbExec(C.Structure):
+    _fields_ = [
+        ("ndevices", C.c_int32),
+        ("devices", C.POINTER(C.c_int32)),
+        ("stream", C.c_void_p),
+        ("flags", C.c_uint32),
+    ]
+
+
+class KronbatchLibraryError(ImportError):
+    pass
+
+
+def _load(path: str = LIB_PATH):
+    if not os.path.exists(path):
+        raise KronbatchLibraryError(
+            f"{path} is missing: build the sm_100a library first (`make lib` or __graft_entry__.build()). "
+            "There is no CPU fallback.")
+    lib = C.CDLL(path)
+    i64, vp, ch = C.c_int64, C.c_void_p, C.c_char
+    for name, T in (("kb_skron2", C.c_float), ("kb_dkron2", C.c_double)):
+        f = getattr(lib, name)
+        f.restype = C.c_int
+        f.argtypes = [ch, ch, ch, i64, i64, i64, i64, i64, T, vp, i64, i64, vp, i64, i64, vp, i64, i64, i64, T, vp,
+                      i64, i64, i64, C.POINTER(KbExec), C.c_char_p, C.c_size_t]
+    for name, T in (("kb_skron3", C.c_float), ("kb_dkron3", C.c_double)):
+        f = getattr(lib, name)
+        f.restype = C.c_int
+        f.argtypes = [ch, ch, ch, i64, i64, i64, i64, i64, i64, i64, T, vp, i64, i64, vp, i64, i64, vp, i64, i64, vp,
+                      i64, i64, i64, i64, T, vp, i64, i64, i64, i64, vp, i64, C.POINTER(KbExec), C.c_char_p,
+                      C.c_size_t]
+    lib.kb_kron3_workspace_size.restype = C.c_int
+    lib.kb_kron3_workspace_size.argtypes = [i64, i64, i64, i64, C.POINTER(i64), C.c_char_p, C.c_size_t]
+    lib.kb_version.restype = C.c_char_p
+    lib.kb_launch_count.restype = C.c_uint64
+    lib.kb_last_path.restype = C.c_char_p
+    lib.kb_release_buffers.restype = None
+    return lib
+
+
+lib = _load()
+
+
+def raise_for(rc: int, err) -> None:
+    if rc == KB_OK:
+        return
+    msg = err.value.decode(errors="replace") if err is not None else ""
+    if rc == KB_EINVAL:
+        raise ValueError(msg)
+    if rc == KB_EOVERFLOW:
+        raise OverflowError(msg)
+    if rc == KB_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg or f"kronbatch_b200 error {rc}")

@@ -1,0 +1,189 @@
+// kb_device.cuh -- device-side building blocks shared by the sm_100a kron kernels.
+//
+// Arithmetic contract (reference detail.hpp:38-117):
+// every accumulation step is ONE IEEE fma in round-to-nearest, performed in
+// ascending contraction index per output element, starting from the beta
+// initialisation (0 / Y / fl(Y*beta)); the right factor is pre-scaled as
+// w = fl(alpha * R). `fma.rn.f32x2` (SASS FFMA2) packs two DIFFERENT output
+// elements per instruction -- never two terms of one sum -- so it preserves
+// the per-element order. Nothing here relies on nvcc's --fmad contraction.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kb {
+
+// ------------------------------------------------------------ arithmetic --
+
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
+// {d.x, d.y} = {fma(a.x, s, c.x), fma(a.y, s, c.y)} as one FFMA2 with a
+// broadcast scalar operand.
+__device__ __forceinline__ float2 ffma2_s(float2 a, float s, float2 c) {
+  unsigned long long ra, rc, rd, rs;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(rs) : "f"(s));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rc) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rs), "l"(rc));
+  float2 d;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+  return d;
+}
+
+// acc[r] = fma(a[r], s, acc[r]) for r < R; pairs go through FFMA2 for float.
+template <int R>
+__device__ __forceinline__ void axpy_rows(float (&acc)[R], const float (&a)[R], float s) {
+#pragma unroll
+  for (int r = 0; r + 1 < R; r += 2) {
+    float2 d = ffma2_s(make_float2(a[r], a[r + 1]), s, make_float2(acc[r], acc[r + 1]));
+    acc[r] = d.x;
+    acc[r + 1] = d.y;
+  }
+  if constexpr (R % 2) acc[R - 1] = __fmaf_rn(a[R - 1], s, acc[R - 1]);
+}
+template <int R>
+__device__ __forceinline__ void axpy_rows(double (&acc)[R], const double (&a)[R], double s) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = __fma_rn(a[r], s, acc[r]);
+}
+
+// -------------------------------------------------------- shared memory --
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gmem_src, bool valid) {
+  const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  const int src_bytes = valid ? BYTES : 0;  // 0 => zero-fill, source not read
+  if constexpr (BYTES == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gmem_src), "r"(src_bytes)
+                 : "memory");
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(dst), "l"(gmem_src), "n"(BYTES),
+                 "r"(src_bytes)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Vector load of W consecutive elements (W*sizeof(T) bytes, naturally aligned).
+template <int W, typename T>
+__device__ __forceinline__ void lds_vec(T* dst, const T* src) {
+  if constexpr (W * sizeof(T) == 16) {
+    if constexpr (sizeof(T) == 4) {
+      float4 v = *reinterpret_cast<const float4*>(src);
+      dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
+    } else {
+      double2 v = *reinterpret_cast<const double2*>(src);
+      dst[0] = v.x; dst[1] = v.y;
+    }
+  } else if constexpr (W * sizeof(T) == 8 && sizeof(T) == 4) {
+    float2 v = *reinterpret_cast<const float2*>(src);
+    dst[0] = v.x; dst[1] = v.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < W; ++i) dst[i] = src[i];
+  }
+}
+
+// Load n consecutive elements with the widest aligned vector width VW.
+template <int n, int VW, typename T>
+__device__ __forceinline__ void lds_n(T* dst, const T* src) {
+  static_assert(n % VW == 0, "vector width must divide the length");
+#pragma unroll
+  for (int i = 0; i < n; i += VW) lds_vec<VW>(dst + i, src + i);
+}
+
+// Store n consecutive elements to global memory with vector width VW.
+template <int n, int VW, typename T>
+__device__ __forceinline__ void stg_n(T* dst, const T* src) {
+#pragma unroll
+  for (int i = 0; i < n; i += VW) {
+    if constexpr (VW * sizeof(T) == 16) {
+      if constexpr (sizeof(T) == 4)
+        *reinterpret_cast<float4*>(dst + i) = make_float4(src[i], src[i + 1], src[i + 2], src[i + 3]);
+      else
+        *reinterpret_cast<double2*>(dst + i) = make_double2(src[i], src[i + 1]);
+    } else if constexpr (VW * sizeof(T) == 8 && sizeof(T) == 4) {
+      *reinterpret_cast<float2*>(dst + i) = make_float2(src[i], src[i + 1]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < VW; ++k) dst[i + k] = src[i + k];
+    }
+  }
+}
+
+template <int n, int VW, typename T>
+__device__ __forceinline__ void ldg_n(T* dst, const T* src) {
+#pragma unroll
+  for (int i = 0; i < n; i += VW) {
+    if constexpr (VW * sizeof(T) == 16) {
+      if constexpr (sizeof(T) == 4) {
+        float4 v = *reinterpret_cast<const float4*>(src + i);
+        dst[i] = v.x; dst[i + 1] = v.y; dst[i + 2] = v.z; dst[i + 3] = v.w;
+      } else {
+        double2 v = *reinterpret_cast<const double2*>(src + i);
+        dst[i] = v.x; dst[i + 1] = v.y;
+      }
+    } else if constexpr (VW * sizeof(T) == 8 && sizeof(T) == 4) {
+      float2 v = *reinterpret_cast<const float2*>(src + i);
+      dst[i] = v.x; dst[i + 1] = v.y;
+    } else {
+#pragma unroll
+      for (int k = 0; k < VW; ++k) dst[i + k] = src[i + k];
+    }
+  }
+}
+
+// --------------------------------------------------------- kernel params --
+
+// beta initialisation classes of gemm_axpy (detail.hpp:45-51)
+enum BetaMode : int { kBetaZero = 0, kBetaOne = 1, kBetaScale = 2 };
+
+template <typename T>
+__device__ __forceinline__ T beta_init(int mode, T beta, T prior) {
+  return mode == kBetaZero ? T(0) : (mode == kBetaOne ? prior : mul_rn(prior, beta));
+}
+
+template <typename T>
+struct Kron2Params {
+  const T* A;
+  const T* B;
+  const T* X;
+  T* Y;
+  long long lda, ldb, ldx, sx, ldy, sy;
+  long long m_a, n_a, m_b, n_b;
+  long long batch;   // entries this launch processes (already offset pointers)
+  int opa, opb, opx; // 1 = transposed
+  int beta_mode;
+  T alpha, beta;
+};
+
+template <typename T>
+struct Kron3Params {
+  const T* A;
+  const T* B;
+  const T* C;
+  const T* X;
+  T* Y;
+  long long lda, ldb, ldc, ldx, ldx2, sx, ldy, ldy2, sy;
+  long long m_a, n_a, m_b, n_b, m_c, n_c;
+  long long batch;
+  int opa, opb, opc;
+  int beta_mode;
+  T alpha, beta;
+};
+
+// op-resolved element (i, j) of a stored matrix: op(M)(i, j)
+template <typename T>
+__device__ __forceinline__ T op_at(const T* m, long long ld, int trans, long long i, long long j) {
+  return trans ? m[j + i * ld] : m[i + j * ld];
+}
+
+}  // namespace kb

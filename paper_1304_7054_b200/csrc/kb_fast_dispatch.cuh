@@ -1,0 +1,145 @@
+// kb_fast_dispatch.cuh -- host-side launch of the square n <= 16 kernels:
+// fast-path preconditions, persistent grid sizing (SM count x resident CTAs),
+// one-time dynamic-smem attribute per instantiation.
+#pragma once
+
+#include <mutex>
+#include <cstdlib>
+#include <map>
+#include <utility>
+
+#include "kb_fast.cuh"
+#include "kb_kernels.h"
+
+namespace kb {
+
+// Resident CTAs per SM for a kernel instantiation; sets its dynamic-smem
+// attribute on first use. Keyed by the kernel's address (all instantiations
+// of one template share a function-pointer type).
+template <typename Kern>
+static int occupancy_for(Kern kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto dkey = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+  auto it = cache.find(dkey);
+  if (it != cache.end()) return it->second;
+  int occ = 0;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    occ = 0;
+  }
+  cache[dkey] = occ;
+  return occ;
+}
+
+template <typename T>
+static bool aligned(const void* p, int elems) {
+  return (reinterpret_cast<uintptr_t>(p) % (sizeof(T) * (size_t)elems)) == 0;
+}
+
+// Development-time variant selection (tools/ sweeps): KB_VARIANT2 / KB_VARIANT3.
+static int env_variant(const char* name) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : 0;
+}
+
+template <typename T, int N, int OPX, int V>
+static cudaError_t launch2v(const Kron2Params<T>& p, int sm_count, cudaStream_t s) {
+  using C = SqCfg<T, N>;
+  using K = Kron2Fast<T, N, V>;
+  if (p.ldx != N || p.sx % C::VXC || !aligned<T>(p.X, C::VXC)) return cudaErrorNotSupported;
+  if (p.ldy % C::VY || p.sy % C::VY || !aligned<T>(p.Y, C::VY)) return cudaErrorNotSupported;
+  auto kern = kron2_sq_kernel<T, N, OPX, V>;
+  const int threads = K::WARPS * 32;
+  const size_t smem = K::smem_bytes();
+  const int occ = occupancy_for(kern, threads, smem);
+  if (occ <= 0) return cudaErrorNotSupported;
+  const long long ngroups = (p.batch + C::IPW - 1) / C::IPW;
+  const long long want = (ngroups + K::WARPS - 1) / K::WARPS;
+  const int grid = (int)(want < (long long)sm_count * occ ? want : (long long)sm_count * occ);
+  kern<<<grid, threads, smem, s>>>(p, ngroups);
+  return cudaGetLastError();
+}
+
+template <typename T, int N, int OPX>
+static cudaError_t launch2(const Kron2Params<T>& p, int sm_count, cudaStream_t s) {
+  if constexpr (N == 10 || N == 16) {
+    static const int v = env_variant("KB_VARIANT2");
+    switch (v) {
+      case 1: return launch2v<T, N, OPX, 1>(p, sm_count, s);
+      case 2: return launch2v<T, N, OPX, 2>(p, sm_count, s);
+      case 3: return launch2v<T, N, OPX, 3>(p, sm_count, s);
+      default: break;
+    }
+  }
+  return launch2v<T, N, OPX, 0>(p, sm_count, s);
+}
+
+template <typename T, int N, int V>
+static cudaError_t launch3v(const Kron3Params<T>& p, int sm_count, cudaStream_t s) {
+  using C = SqCfg<T, N>;
+  using K = Kron3Fast<T, N, V>;
+  if (p.ldx != N || p.ldx2 != (long long)N * N || p.sx % C::VXC || !aligned<T>(p.X, C::VXC))
+    return cudaErrorNotSupported;
+  if (p.ldy % C::VY || p.ldy2 % C::VY || p.sy % C::VY || !aligned<T>(p.Y, C::VY)) return cudaErrorNotSupported;
+  auto kern = kron3_sq_kernel<T, N, V>;
+  const size_t smem = K::smem_bytes();
+  const int occ = occupancy_for(kern, K::THREADS, smem);
+  if (occ <= 0) return cudaErrorNotSupported;
+  const long long ntiles = (p.batch + K::IT - 1) / K::IT;
+  const int grid = (int)(ntiles < (long long)sm_count * occ ? ntiles : (long long)sm_count * occ);
+  kern<<<grid, K::THREADS, smem, s>>>(p, ntiles);
+  return cudaGetLastError();
+}
+
+template <typename T, int N>
+static cudaError_t launch3(const Kron3Params<T>& p, int sm_count, cudaStream_t s) {
+  if constexpr (N == 10 || N == 16) {
+    static const int v = env_variant("KB_VARIANT3");
+    switch (v) {
+      case 1: return launch3v<T, N, 1>(p, sm_count, s);
+      case 2: return launch3v<T, N, 2>(p, sm_count, s);
+      case 3: return launch3v<T, N, 3>(p, sm_count, s);
+      default: break;
+    }
+  }
+  return launch3v<T, N, 0>(p, sm_count, s);
+}
+
+#define KB_CASE2(N)                                                    \
+  case N:                                                              \
+    return p.opx ? launch2<T, N, 1>(p, sm_count, s) : launch2<T, N, 0>(p, sm_count, s);
+#define KB_CASE3(N) \
+  case N:           \
+    return launch3<T, N>(p, sm_count, s);
+
+template <typename T>
+cudaError_t launch_kron2_fast(const Kron2Params<T>& p, int sm_count, cudaStream_t s) {
+  if (p.m_a != p.n_a || p.m_a != p.m_b || p.m_a != p.n_b) return cudaErrorNotSupported;
+  switch (p.m_a) {
+    KB_CASE2(1) KB_CASE2(2) KB_CASE2(3) KB_CASE2(4) KB_CASE2(5) KB_CASE2(6) KB_CASE2(7) KB_CASE2(8)
+    KB_CASE2(9) KB_CASE2(10) KB_CASE2(11) KB_CASE2(12) KB_CASE2(13) KB_CASE2(14) KB_CASE2(15) KB_CASE2(16)
+    default: return cudaErrorNotSupported;
+  }
+}
+
+template <typename T>
+cudaError_t launch_kron3_fast(const Kron3Params<T>& p, int sm_count, cudaStream_t s) {
+  if (p.m_a != p.n_a || p.m_a != p.m_b || p.m_a != p.n_b || p.m_a != p.m_c || p.m_a != p.n_c)
+    return cudaErrorNotSupported;
+  switch (p.m_a) {
+    KB_CASE3(1) KB_CASE3(2) KB_CASE3(3) KB_CASE3(4) KB_CASE3(5) KB_CASE3(6) KB_CASE3(7) KB_CASE3(8)
+    KB_CASE3(9) KB_CASE3(10) KB_CASE3(11) KB_CASE3(12) KB_CASE3(13) KB_CASE3(14) KB_CASE3(15) KB_CASE3(16)
+    default: return cudaErrorNotSupported;
+  }
+}
+
+#undef KB_CASE2
+#undef KB_CASE3
+
+}  // namespace kb

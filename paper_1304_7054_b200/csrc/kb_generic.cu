@@ -1,0 +1,153 @@
+// kb_generic.cu -- general-shape sm_100a kernels for kron2 / kron3.
+//
+// These cover every shape, op and stride combination the reference API
+// accepts (rectangular, n > 16, padded leading dimensions / batch strides,
+// ConjTranspose == Transpose). They follow the reference contraction exactly
+// (kron2.hpp:95-107, kron3.hpp:147-163, detail.hpp:38-117):
+//   kron2: tmp(i,c) = sum_l A_r(i,l) Xop(l,c)                (init 0, l ascending)
+//          Y(i,j)  = init + sum_m tmp(i,m) * fl(alpha*B_r(j,m)) (m ascending)
+//   kron3: per plane N: t1 = A_r X(:,:,N);  T2(:,:,N) = t1 B_r^T  (alpha 1, beta 0)
+//          Y(i,j,k) = init + sum_N T2(i,j,N) * fl(alpha*C_r(k,N))
+// One CTA owns one batch entry at a time (grid-stride over entries); the
+// per-entry intermediates live in shared memory when they fit, otherwise in a
+// per-CTA slice of a device scratch buffer (the library's internal pool; the
+// caller's kron3 Workspace is not touched -- it is a CPU-path artefact).
+// The square n <= 16 fast paths are in kb_fast.cu.
+#include "kb_device.cuh"
+#include "kb_kernels.h"
+
+namespace kb {
+
+template <typename T>
+__global__ void __launch_bounds__(256) kron2_generic_kernel(Kron2Params<T> p, T* scratch, int use_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const long long tsz = p.m_a * p.n_b;
+  T* tmp = use_smem ? reinterpret_cast<T*>(smem_raw) : scratch + (long long)blockIdx.x * tsz;
+  const long long ysz = p.m_a * p.m_b;
+  for (long long e = blockIdx.x; e < p.batch; e += gridDim.x) {
+    const T* x = p.X + e * p.sx;
+    T* y = p.Y + e * p.sy;
+    // stage 1: tmp = op(A) * op(X^e)    (kron2.hpp:96-103)
+    for (long long t = threadIdx.x; t < tsz; t += blockDim.x) {
+      const long long i = t % p.m_a, c = t / p.m_a;
+      T acc = T(0);
+      for (long long l = 0; l < p.n_a; ++l)
+        acc = fma_rn(op_at(p.A, p.lda, p.opa, i, l), op_at(x, p.ldx, p.opx, l, c), acc);
+      tmp[t] = acc;
+    }
+    __syncthreads();
+    // stage 2: Y = alpha * tmp * op(B)^T + beta * Y    (kron2.hpp:105-107)
+    for (long long t = threadIdx.x; t < ysz; t += blockDim.x) {
+      const long long i = t % p.m_a, j = t / p.m_a;
+      T* yij = y + i + j * p.ldy;
+      T acc = beta_init(p.beta_mode, p.beta, p.beta_mode == kBetaZero ? T(0) : *yij);
+      for (long long m = 0; m < p.n_b; ++m)
+        acc = fma_rn(tmp[i + m * p.m_a], mul_rn(p.alpha, op_at(p.B, p.ldb, p.opb, j, m)), acc);
+      *yij = acc;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) kron3_generic_kernel(Kron3Params<T> p, T* scratch, int use_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const long long t1sz = p.m_a * p.n_b;
+  const long long t2sz = p.m_a * p.m_b * p.n_c;
+  T* base = use_smem ? reinterpret_cast<T*>(smem_raw) : scratch + (long long)blockIdx.x * (t1sz + t2sz);
+  T* t1 = base;
+  T* t2 = base + t1sz;
+  const long long mab = p.m_a * p.m_b;
+  const long long ysz = mab * p.m_c;
+  for (long long e = blockIdx.x; e < p.batch; e += gridDim.x) {
+    const T* x = p.X + e * p.sx;
+    T* y = p.Y + e * p.sy;
+    // stage 1 per plane (kron3.hpp:147-156)
+    for (long long N = 0; N < p.n_c; ++N) {
+      const T* xp = x + N * p.ldx2;
+      for (long long t = threadIdx.x; t < t1sz; t += blockDim.x) {
+        const long long i = t % p.m_a, c = t / p.m_a;
+        T acc = T(0);
+        for (long long l = 0; l < p.n_a; ++l) acc = fma_rn(op_at(p.A, p.lda, p.opa, i, l), xp[l + c * p.ldx], acc);
+        t1[t] = acc;
+      }
+      __syncthreads();
+      T* t2p = t2 + N * mab;
+      for (long long t = threadIdx.x; t < mab; t += blockDim.x) {
+        const long long i = t % p.m_a, j = t / p.m_a;
+        T acc = T(0);
+        for (long long m = 0; m < p.n_b; ++m) acc = fma_rn(t1[i + m * p.m_a], op_at(p.B, p.ldb, p.opb, j, m), acc);
+        t2p[t] = acc;
+      }
+      __syncthreads();
+    }
+    // stage 2: Y(:,j,:) = alpha * T2(:,j,:) * op(C)^T + beta * Y   (kron3.hpp:158-163)
+    for (long long t = threadIdx.x; t < ysz; t += blockDim.x) {
+      const long long i = t % p.m_a, j = (t / p.m_a) % p.m_b, k = t / mab;
+      T* yv = y + i + j * p.ldy + k * p.ldy2;
+      T acc = beta_init(p.beta_mode, p.beta, p.beta_mode == kBetaZero ? T(0) : *yv);
+      for (long long N = 0; N < p.n_c; ++N)
+        acc = fma_rn(t2[i + j * p.m_a + N * mab], mul_rn(p.alpha, op_at(p.C, p.ldc, p.opc, k, N)), acc);
+      *yv = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// Y <- init(beta) only: the empty-sum / alpha == 0 path (kron2.hpp:67-79,
+// kron3.hpp:113-128). A, B, C, X are never read. Element (i, j[, k]) of entry e.
+template <typename T>
+__global__ void __launch_bounds__(256) scale_kernel(T* Y, long long batch, long long d1, long long d2, long long d3,
+                                                    long long ld, long long ld2, long long sy, int beta_mode,
+                                                    T beta) {
+  const long long per = d1 * d2 * d3;
+  const long long total = per * batch;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long e = t / per, r = t % per;
+    const long long i = r % d1, j = (r / d1) % d2, k = r / (d1 * d2);
+    T* y = Y + e * sy + i + j * ld + k * ld2;
+    *y = beta_mode == kBetaZero ? T(0) : mul_rn(*y, beta);
+  }
+}
+
+// ---------------------------------------------------------------- launch --
+
+template <typename T>
+cudaError_t launch_kron2_generic(const Kron2Params<T>& p, T* scratch, long long scratch_elems, int grid,
+                                 cudaStream_t s) {
+  const size_t tbytes = sizeof(T) * (size_t)(p.m_a * p.n_b);
+  const int use_smem = tbytes <= 48 * 1024;
+  if (!use_smem && scratch_elems < (long long)grid * p.m_a * p.n_b) return cudaErrorInvalidValue;
+  kron2_generic_kernel<T><<<grid, 256, use_smem ? tbytes : 0, s>>>(p, scratch, use_smem);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_kron3_generic(const Kron3Params<T>& p, T* scratch, long long scratch_elems, int grid,
+                                 cudaStream_t s) {
+  const long long elems = p.m_a * p.n_b + p.m_a * p.m_b * p.n_c;
+  const size_t tbytes = sizeof(T) * (size_t)elems;
+  const int use_smem = tbytes <= 48 * 1024;
+  if (!use_smem && scratch_elems < (long long)grid * elems) return cudaErrorInvalidValue;
+  kron3_generic_kernel<T><<<grid, 256, use_smem ? tbytes : 0, s>>>(p, scratch, use_smem);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_scale(T* Y, long long batch, long long d1, long long d2, long long d3, long long ld,
+                         long long ld2, long long sy, int beta_mode, T beta, int grid, cudaStream_t s) {
+  scale_kernel<T><<<grid, 256, 0, s>>>(Y, batch, d1, d2, d3, ld, ld2, sy, beta_mode, beta);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_kron2_generic<float>(const Kron2Params<float>&, float*, long long, int, cudaStream_t);
+template cudaError_t launch_kron2_generic<double>(const Kron2Params<double>&, double*, long long, int, cudaStream_t);
+template cudaError_t launch_kron3_generic<float>(const Kron3Params<float>&, float*, long long, int, cudaStream_t);
+template cudaError_t launch_kron3_generic<double>(const Kron3Params<double>&, double*, long long, int, cudaStream_t);
+template cudaError_t launch_scale<float>(float*, long long, long long, long long, long long, long long, long long,
+                                         long long, int, float, int, cudaStream_t);
+template cudaError_t launch_scale<double>(double*, long long, long long, long long, long long, long long, long long,
+                                          long long, int, double, int, cudaStream_t);
+
+}  // namespace kb

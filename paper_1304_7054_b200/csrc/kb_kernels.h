@@ -1,0 +1,34 @@
+// kb_kernels.h -- internal launch interface between the host runtime
+// (kb_runtime.cu) and the sm_100a kernels (kb_generic.cu, kb_fast*.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "kb_device.cuh"
+
+namespace kb {
+
+// Shape-generic kernels: any dims / ops / strides. `scratch` (grid * per-CTA
+// intermediate elements) is only used when the per-entry intermediates exceed
+// the 48 KiB shared-memory budget.
+template <typename T>
+cudaError_t launch_kron2_generic(const Kron2Params<T>& p, T* scratch, long long scratch_elems, int grid,
+                                 cudaStream_t s);
+template <typename T>
+cudaError_t launch_kron3_generic(const Kron3Params<T>& p, T* scratch, long long scratch_elems, int grid,
+                                 cudaStream_t s);
+// Y <- init(beta) for the alpha == 0 / empty-sum path.
+template <typename T>
+cudaError_t launch_scale(T* Y, long long batch, long long d1, long long d2, long long d3, long long ld,
+                         long long ld2, long long sy, int beta_mode, T beta, int grid, cudaStream_t s);
+
+// Square n <= 16 register-blocked kernels. Return cudaErrorNotSupported
+// (without launching) when the layout does not meet the fast-path
+// preconditions (tight entries, vector alignment); the caller then uses the
+// generic kernel.
+template <typename T>
+cudaError_t launch_kron2_fast(const Kron2Params<T>& p, int sm_count, cudaStream_t s);
+template <typename T>
+cudaError_t launch_kron3_fast(const Kron3Params<T>& p, int sm_count, cudaStream_t s);
+
+}  // namespace kb

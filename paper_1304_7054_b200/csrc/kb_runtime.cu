@@ -1,0 +1,634 @@
+// kb_runtime.cu -- the C ABI (include/kronbatch_b200.h): validation with the
+// reference's exact messages, pointer classification, the device-buffer
+// manager (per-thread, per-device pooled buffers and streams), the staged
+// host-buffer pipeline, batch sharding over several GPUs, and kernel dispatch.
+//
+// Replaces the reference's L1 execution layer:
+//   detail::run_chunked / chunk_entries_for  detail.hpp:140-180  (OpenMP batch
+//     launcher)        -> persistent sm_100a grids + per-GPU contiguous slices
+//   detail::resolve_op detail.hpp:19-31 -> resolved per CTA into smem
+//   detail::gemm_axpy  detail.hpp:38-117 -> kb_fast.cuh / kb_generic.cu
+// and keeps L0 validation semantics (views.hpp:172-240) and the L2 control
+// flow (kron2.hpp:41-79, kron3.hpp:77-128) bit-for-bit in behaviour.
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/kronbatch_b200.h"
+#include "kb_kernels.h"
+
+namespace {
+
+using kb::Kron2Params;
+using kb::Kron3Params;
+using i64 = int64_t;
+
+std::atomic<uint64_t> g_launches{0};
+thread_local std::string t_last_path;
+
+// ------------------------------------------------------------ errors -----
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+int report(const Fail& f, char* err, size_t errlen) {
+  if (err && errlen) {
+    std::strncpy(err, f.msg.c_str(), errlen - 1);
+    err[errlen - 1] = 0;
+  }
+  return f.code;
+}
+
+std::string nums(i64 a, i64 b) { return "(" + std::to_string(a) + ") < (" + std::to_string(b) + ")"; }
+
+[[noreturn]] void layout_error(const std::string& ctx, const std::string& what) {
+  throw Fail{KB_EINVAL, ctx.empty() ? what : ctx + ": " + what};
+}
+
+void cuda_check(cudaError_t e, const char* ctx) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Fail{e == cudaErrorMemoryAllocation ? KB_ENOMEM : KB_ECUDA,
+               std::string(ctx) + ": CUDA error: " + cudaGetErrorString(e)};
+  }
+}
+
+// ------------------------------------------- validation (views.hpp) -----
+
+i64 fp_matrix(i64 cols, i64 ld) { return cols == 0 ? 0 : ld * cols; }
+i64 fp_array3(i64 d3, i64 ld2) { return d3 == 0 ? 0 : ld2 * d3; }
+
+// validate(MatrixView) views.hpp:198-209
+void validate_matrix(const std::string& ctx, i64 rows, i64 cols, i64 ld, i64 len) {
+  if (rows < 0 || cols < 0) layout_error(ctx, "negative rows/cols");
+  if (ld < std::max<i64>(rows, 1)) layout_error(ctx, "ld " + nums(ld, std::max<i64>(rows, 1)));
+  if (len < fp_matrix(cols, ld)) layout_error(ctx, "buffer length " + nums(len, fp_matrix(cols, ld)));
+}
+
+// validate(Array3View) views.hpp:211-223
+void validate_array3(const std::string& ctx, i64 d1, i64 d2, i64 d3, i64 ld, i64 ld2, i64 len) {
+  if (d1 < 0 || d2 < 0 || d3 < 0) layout_error(ctx, "negative dims");
+  if (ld < std::max<i64>(d1, 1)) layout_error(ctx, "ld " + nums(ld, std::max<i64>(d1, 1)));
+  if (ld2 < ld * d2) layout_error(ctx, "ld2 " + nums(ld2, ld * d2));
+  if (len < fp_array3(d3, ld2)) layout_error(ctx, "buffer length " + nums(len, fp_array3(d3, ld2)));
+}
+
+// validate_batch views.hpp:225-240 (base already described by the caller)
+template <typename ValidateBase>
+void validate_batch(const std::string& ctx, i64 count, i64 stride, i64 fp, i64 len, ValidateBase&& vb) {
+  if (count < 0) layout_error(ctx, "negative batch_count");
+  if (count == 0) return;
+  vb();
+  if (stride < fp) layout_error(ctx, "batch_stride " + nums(stride, fp) + ", batch_stride < entry footprint");
+  const i64 needed = (count - 1) * stride + fp;
+  if (len < needed)
+    layout_error(ctx, "buffer length " + nums(len, needed) + " for " + std::to_string(count) + " entries");
+}
+
+int is_t(char op) { return op != 'N' && op != 'n'; }
+void check_op(const char* ctx, char op) {
+  if (!(op == 'N' || op == 'n' || op == 'T' || op == 't' || op == 'C' || op == 'c'))
+    layout_error(ctx, std::string("invalid op '") + op + "'");
+}
+
+// ------------------------------------------------ device-buffer manager ---
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes <= cap) return p;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max(bytes, cap * 3 / 2);
+    cuda_check(cudaMalloc(&p, want), "device buffer");
+    cap = want;
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+constexpr int kSlots = 3;  // staged pipeline depth (chunks in flight)
+
+struct DevRes {
+  int device = -1;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;        // library stream
+  cudaStream_t slot_stream[kSlots] = {};  // staged pipeline streams
+  Buf consts;
+  Buf scratch[kSlots];
+  Buf xs[kSlots], ys[kSlots];
+};
+
+struct ThreadRes {
+  std::unordered_map<int, DevRes*> by_dev;
+  ~ThreadRes() {
+    // streams/buffers are intentionally not destroyed at thread exit: the CUDA
+    // runtime may already be torn down at process exit (kb_release_buffers()
+    // frees them explicitly).
+  }
+};
+thread_local ThreadRes t_res;
+
+DevRes& dev_res(int dev) {
+  auto it = t_res.by_dev.find(dev);
+  if (it != t_res.by_dev.end()) return *it->second;
+  auto* r = new DevRes;
+  r->device = dev;
+  cuda_check(cudaDeviceGetAttribute(&r->sm_count, cudaDevAttrMultiProcessorCount, dev), "device query");
+  cuda_check(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking), "stream");
+  for (auto& s : r->slot_stream) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  t_res.by_dev[dev] = r;
+  return *r;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev != prev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---------------------------------------------------- pointer classes ----
+
+struct PtrInfo {
+  bool device = false;  // dereferenceable by kernels (device or managed)
+  int dev = -1;
+  bool pinned = false;
+};
+
+PtrInfo classify(const void* p) {
+  PtrInfo r;
+  if (!p) return r;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return r;
+  }
+  switch (a.type) {
+    case cudaMemoryTypeDevice: r.device = true; r.dev = a.device; break;
+    case cudaMemoryTypeManaged: r.device = true; r.dev = a.device; break;
+    case cudaMemoryTypeHost: r.pinned = true; break;
+    default: break;
+  }
+  return r;
+}
+
+int beta_mode_of(double beta) { return beta == 0.0 ? kb::kBetaZero : (beta == 1.0 ? kb::kBetaOne : kb::kBetaScale); }
+
+// Small constant matrix: use in place if device-resident on `dev`, else upload.
+template <typename T>
+const T* const_on_device(const T* m, i64 elems, int dev, T* slot, cudaStream_t s) {
+  const PtrInfo pi = classify(m);
+  if (pi.device && pi.dev == dev) return m;
+  cuda_check(cudaMemcpyAsync(slot, m, sizeof(T) * (size_t)elems, cudaMemcpyDefault, s), "constant upload");
+  return slot;
+}
+
+void count_launch(const char* path) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  t_last_path = path;
+}
+
+// --------------------------------------------------------- kron2 ---------
+
+template <typename T>
+struct K2 {
+  char ta, tb, tx;
+  i64 m_a, n_a, m_b, n_b, batch;
+  T alpha, beta;
+  const T* A; i64 lda;
+  const T* B; i64 ldb;
+  const T* X; i64 ldx, sx, fpx;
+  T* Y; i64 ldy, sy, fpy;
+};
+
+// Launch the compute for entries [0, n) of device-resident X/Y views.
+template <typename T>
+void run2_device(const K2<T>& k, const T* A, const T* B, const T* X, T* Y, i64 n, DevRes& r, cudaStream_t s,
+                 int slot) {
+  Kron2Params<T> p{};
+  p.A = A; p.B = B; p.X = X; p.Y = Y;
+  p.lda = k.lda; p.ldb = k.ldb; p.ldx = k.ldx; p.sx = k.sx; p.ldy = k.ldy; p.sy = k.sy;
+  p.m_a = k.m_a; p.n_a = k.n_a; p.m_b = k.m_b; p.n_b = k.n_b;
+  p.batch = n;
+  p.opa = is_t(k.ta); p.opb = is_t(k.tb); p.opx = is_t(k.tx);
+  p.beta_mode = beta_mode_of((double)k.beta);
+  p.alpha = k.alpha; p.beta = k.beta;
+  cudaError_t e = kb::launch_kron2_fast<T>(p, r.sm_count, s);
+  if (e == cudaSuccess) {
+    count_launch("kron2_fast");
+    return;
+  }
+  if (e != cudaErrorNotSupported) cuda_check(e, "kron2");
+  cudaGetLastError();
+  const int grid = (int)std::min<i64>(n, (i64)r.sm_count * 8);
+  const i64 per = k.m_a * k.n_b;
+  T* scratch = nullptr;
+  i64 scratch_elems = 0;
+  if ((size_t)per * sizeof(T) > 48 * 1024) {
+    scratch_elems = per * grid;
+    scratch = static_cast<T*>(r.scratch[slot].get(sizeof(T) * (size_t)scratch_elems));
+  }
+  cuda_check(kb::launch_kron2_generic<T>(p, scratch, scratch_elems, grid, s), "kron2");
+  count_launch("kron2_generic");
+}
+
+template <typename T>
+void scale2_device(const K2<T>& k, T* Y, i64 n, DevRes& r, cudaStream_t s) {
+  const int mode = beta_mode_of((double)k.beta);
+  if (mode == kb::kBetaOne) return;  // Y <- Y (reference rewrites the same value)
+  const int grid = (int)std::max<i64>(1, std::min<i64>((n * k.m_a * k.m_b + 255) / 256, (i64)r.sm_count * 16));
+  cuda_check(kb::launch_scale<T>(Y, n, k.m_a, k.m_b, 1, k.ldy, 0, k.sy, mode, k.beta, grid, s), "kron2");
+  count_launch("scale");
+}
+
+// Generic driver shared by kron2/kron3: runs entries [p0, p1) on device `dev`,
+// staging host-resident X/Y through pooled device buffers in chunks.
+// `compute(Xd, Yd, n, res, stream)` launches on device-resident views whose
+// entry 0 is the chunk's first entry; `scale_only` selects the Y <- beta*Y path.
+struct StageSpec {
+  i64 sx, fpx, sy, fpy;  // strides / footprints (elements)
+  bool y_in;             // copy Y span in before compute (beta != 0 or padded Y)
+  bool x_used;           // X is read
+  size_t es;             // element size
+};
+
+// `prep(res, stream)` runs once per slice before any compute (constant
+// upload); `compute(Xd, Yd, n, res, stream, slot)` launches the kernel(s).
+template <typename Prep, typename Compute>
+void run_slice(int dev, const void* X, void* Y, i64 p0, i64 p1, const StageSpec& sp, bool x_dev, bool y_dev,
+               cudaStream_t user_stream, bool sync, Prep&& prep, Compute&& compute) {
+  DeviceGuard g(dev);
+  DevRes& r = dev_res(dev);
+  if (p1 <= p0) return;
+  const char* Xb = static_cast<const char*>(X);
+  char* Yb = static_cast<char*>(Y);
+  if ((x_dev || !sp.x_used) && y_dev) {
+    cudaStream_t s = user_stream ? user_stream : r.stream;
+    prep(r, s);
+    compute(sp.x_used ? Xb + sp.es * (size_t)(p0 * sp.sx) : nullptr, Yb + sp.es * (size_t)(p0 * sp.sy), p1 - p0, r,
+            s, 0);
+    if (sync) cuda_check(cudaStreamSynchronize(s), "synchronize");
+    return;
+  }
+  prep(r, r.slot_stream[0]);
+  cuda_check(cudaStreamSynchronize(r.slot_stream[0]), "synchronize");
+  // staged: chunk so one slot holds ~64 MiB of X+Y
+  const i64 per_entry = (sp.x_used && !x_dev ? sp.sx : 0) + (!y_dev ? sp.sy : 0);
+  const i64 target = (64ll << 20) / (i64)sp.es;
+  i64 chunk = std::max<i64>(1, per_entry > 0 ? target / per_entry : (p1 - p0));
+  chunk = std::min(chunk, p1 - p0);
+  if (user_stream) cuda_check(cudaStreamSynchronize(user_stream), "synchronize");
+  i64 c = 0;
+  for (i64 q0 = p0; q0 < p1; q0 += chunk, ++c) {
+    const i64 q1 = std::min(p1, q0 + chunk), n = q1 - q0;
+    const int slot = (int)(c % kSlots);
+    cudaStream_t s = r.slot_stream[slot];
+    const char* xd = nullptr;
+    if (sp.x_used) {
+      const char* xsrc = Xb + sp.es * (size_t)(q0 * sp.sx);
+      if (x_dev) {
+        xd = xsrc;
+      } else {
+        const size_t bytes = sp.es * (size_t)((n - 1) * sp.sx + sp.fpx);
+        void* d = r.xs[slot].get(bytes);
+        cuda_check(cudaMemcpyAsync(d, xsrc, bytes, cudaMemcpyHostToDevice, s), "X upload");
+        xd = static_cast<const char*>(d);
+      }
+    }
+    char* ysrc = Yb + sp.es * (size_t)(q0 * sp.sy);
+    char* yd = ysrc;
+    const size_t ybytes = sp.es * (size_t)((n - 1) * sp.sy + sp.fpy);
+    if (!y_dev) {
+      yd = static_cast<char*>(r.ys[slot].get(ybytes));
+      if (sp.y_in) cuda_check(cudaMemcpyAsync(yd, ysrc, ybytes, cudaMemcpyHostToDevice, s), "Y upload");
+    }
+    compute(xd, yd, n, r, s, slot);
+    if (!y_dev) cuda_check(cudaMemcpyAsync(ysrc, yd, ybytes, cudaMemcpyDeviceToHost, s), "Y download");
+  }
+  for (int k = 0; k < kSlots; ++k) cuda_check(cudaStreamSynchronize(r.slot_stream[k]), "synchronize");
+}
+
+// Shard [0, batch) over devices (contiguous slices), one host thread per GPU.
+template <typename Slice>
+void shard(const kb_exec* exec, int default_dev, i64 batch, Slice&& slice) {
+  std::vector<int> devs;
+  if (exec && exec->ndevices > 1 && exec->devices) {
+    devs.assign(exec->devices, exec->devices + exec->ndevices);
+  } else {
+    devs.push_back(exec && exec->ndevices == 1 && exec->devices ? exec->devices[0] : default_dev);
+  }
+  const i64 G = (i64)devs.size();
+  if (G == 1) {
+    slice(devs[0], 0, batch);
+    return;
+  }
+  const i64 per = (batch + G - 1) / G;
+  std::vector<std::thread> th;
+  std::vector<Fail> fails(G, Fail{KB_OK, {}});
+  for (i64 g = 0; g < G; ++g) {
+    const i64 p0 = std::min(batch, g * per), p1 = std::min(batch, (g + 1) * per);
+    th.emplace_back([&, g, p0, p1] {
+      try {
+        slice(devs[g], p0, p1);
+      } catch (const Fail& f) {
+        fails[g] = f;
+      } catch (const std::exception& e) {
+        fails[g] = Fail{KB_EINTERNAL, e.what()};
+      }
+    });
+  }
+  for (auto& t : th) t.join();  // host barrier: the call returns with every slice done
+  for (auto& f : fails)
+    if (f.code != KB_OK) throw f;
+}
+
+int current_device() {
+  int d = 0;
+  cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+  return d;
+}
+
+template <typename T>
+int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i64 batch, T alpha, const T* A,
+                i64 lda, i64 lena, const T* B, i64 ldb, i64 lenb, const T* X, i64 ldx, i64 ldxp, i64 lenx, T beta,
+                T* Y, i64 ldy, i64 ldyp, i64 leny, const kb_exec* exec, char* err, size_t errlen) {
+  t_last_path.clear();
+  try {
+    check_op("kron2: A", ta);
+    check_op("kron2: B", tb);
+    check_op("kron2: X", tx);
+    // stored shapes implied by the ops (the op(M) dims are m_* x n_*)
+    const i64 ar = is_t(ta) ? n_a : m_a, ac = is_t(ta) ? m_a : n_a;
+    const i64 br = is_t(tb) ? n_b : m_b, bc = is_t(tb) ? m_b : n_b;
+    const i64 xr = is_t(tx) ? n_b : n_a, xc = is_t(tx) ? n_a : n_b;
+    // kron2.hpp:41-44
+    validate_matrix("kron2: A", ar, ac, lda, lena);
+    validate_matrix("kron2: B", br, bc, ldb, lenb);
+    const i64 fpx = fp_matrix(xc, ldx), fpy = fp_matrix(m_b, ldy);
+    validate_batch("kron2: X", batch, ldxp, fpx, lenx, [&] { validate_matrix("kron2: X", xr, xc, ldx, lenx); });
+    validate_batch("kron2: Y", batch, ldyp, fpy, leny, [&] { validate_matrix("kron2: Y", m_a, m_b, ldy, leny); });
+    // kron2.hpp:64-65
+    if (batch == 0 || m_a == 0 || m_b == 0) return KB_OK;
+    const bool scale_only = alpha == T(0) || n_a == 0 || n_b == 0;  // kron2.hpp:67
+    if (scale_only && beta == T(1)) return KB_OK;
+
+    K2<T> k{ta, tb, tx, m_a, n_a, m_b, n_b, batch, alpha, beta, A, lda, B, ldb, X, ldx, ldxp, fpx, Y, ldy, ldyp, fpy};
+    const PtrInfo xi = classify(X), yi = classify(Y);
+    const bool x_dev = !scale_only && xi.device, y_dev = yi.device;
+    const int dev0 = y_dev ? yi.dev : (x_dev ? xi.dev : current_device());
+    const bool y_tight = ldy == m_a && ldyp == m_a * m_b;
+    StageSpec sp{ldxp, fpx, ldyp, fpy, beta != T(0) || !y_tight, !scale_only, sizeof(T)};
+    cudaStream_t us = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
+    const bool sync = !(exec && (exec->flags & KB_EXEC_ASYNC) && x_dev && y_dev);
+    auto slice = [&](int dev, i64 p0, i64 p1) {
+      const T* Ad = nullptr;
+      const T* Bd = nullptr;
+      run_slice(
+          dev, X, Y, p0, p1, sp, x_dev && xi.dev == dev, y_dev && yi.dev == dev, us, sync,
+          [&](DevRes& r, cudaStream_t s) {
+            if (scale_only) return;  // A, B never read (kron2.hpp:67-79)
+            const i64 fa = fp_matrix(ac, lda), fb = fp_matrix(bc, ldb);
+            T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + fb + 64)));
+            Ad = const_on_device(A, fa, r.device, cs, s);
+            Bd = const_on_device(B, fb, r.device, cs + fa + 32, s);
+          },
+          [&](const void* xd, void* yd, i64 n, DevRes& r, cudaStream_t s, int slot) {
+            if (scale_only)
+              scale2_device<T>(k, static_cast<T*>(yd), n, r, s);
+            else
+              run2_device<T>(k, Ad, Bd, static_cast<const T*>(xd), static_cast<T*>(yd), n, r, s, slot);
+          });
+    };
+    if (x_dev || y_dev)
+      slice(dev0, 0, batch);  // device-resident data runs where it lives
+    else
+      shard(exec, dev0, batch, slice);
+    return KB_OK;
+  } catch (const Fail& f) {
+    return report(f, err, errlen);
+  } catch (const std::exception& e) {
+    return report(Fail{KB_EINTERNAL, std::string("kron2: ") + e.what()}, err, errlen);
+  }
+}
+
+// --------------------------------------------------------- kron3 ---------
+
+template <typename T>
+int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i64 m_c, i64 n_c, i64 batch, T alpha,
+                const T* A, i64 lda, i64 lena, const T* B, i64 ldb, i64 lenb, const T* Cm, i64 ldc, i64 lenc,
+                const T* X, i64 ldx, i64 ldx2, i64 ldxp, i64 lenx, T beta, T* Y, i64 ldy, i64 ldy2, i64 ldyp,
+                i64 leny, T* work, i64 work_cap, const kb_exec* exec, char* err, size_t errlen) {
+  (void)work;
+  t_last_path.clear();
+  try {
+    check_op("kron3: A", ta);
+    check_op("kron3: B", tb);
+    check_op("kron3: C", tc);
+    const i64 ar = is_t(ta) ? n_a : m_a, ac = is_t(ta) ? m_a : n_a;
+    const i64 br = is_t(tb) ? n_b : m_b, bc = is_t(tb) ? m_b : n_b;
+    const i64 cr = is_t(tc) ? n_c : m_c, cc = is_t(tc) ? m_c : n_c;
+    // kron3.hpp:77-81
+    validate_matrix("kron3: A", ar, ac, lda, lena);
+    validate_matrix("kron3: B", br, bc, ldb, lenb);
+    validate_matrix("kron3: C", cr, cc, ldc, lenc);
+    const i64 fpx = fp_array3(n_c, ldx2), fpy = fp_array3(m_c, ldy2);
+    validate_batch("kron3: X", batch, ldxp, fpx, lenx,
+                   [&] { validate_array3("kron3: X", n_a, n_b, n_c, ldx, ldx2, lenx); });
+    validate_batch("kron3: Y", batch, ldyp, fpy, leny,
+                   [&] { validate_array3("kron3: Y", m_a, m_b, m_c, ldy, ldy2, leny); });
+    // kron3_workspace_size + capacity check before any exit (kron3.hpp:104-109)
+    if (m_a < 0 || m_b < 0 || n_c < 0 || batch < 0)
+      throw Fail{KB_EINVAL, "kron3_workspace_size: negative dimension"};
+    i64 needed = m_a;
+    for (i64 f : {m_b, n_c, batch})
+      if (__builtin_mul_overflow(needed, f, &needed))
+        throw Fail{KB_EOVERFLOW, "kron3_workspace_size: m_a*m_b*n_c*batch_count overflows"};
+    if (work_cap < needed)
+      layout_error("kron3: workspace",
+                   "too small: need " + std::to_string(needed) + " elements, got " + std::to_string(work_cap));
+    if (batch == 0 || m_a == 0 || m_b == 0 || m_c == 0) return KB_OK;  // kron3.hpp:111
+    const bool scale_only = alpha == T(0) || n_a == 0 || n_b == 0 || n_c == 0;  // kron3.hpp:113
+    if (scale_only && beta == T(1)) return KB_OK;
+
+    Kron3Params<T> base{};
+    base.lda = lda; base.ldb = ldb; base.ldc = ldc;
+    base.ldx = ldx; base.ldx2 = ldx2; base.sx = ldxp;
+    base.ldy = ldy; base.ldy2 = ldy2; base.sy = ldyp;
+    base.m_a = m_a; base.n_a = n_a; base.m_b = m_b; base.n_b = n_b; base.m_c = m_c; base.n_c = n_c;
+    base.opa = is_t(ta); base.opb = is_t(tb); base.opc = is_t(tc);
+    base.beta_mode = beta_mode_of((double)beta);
+    base.alpha = alpha; base.beta = beta;
+
+    const PtrInfo xi = classify(X), yi = classify(Y);
+    const bool x_dev = !scale_only && xi.device, y_dev = yi.device;
+    const int dev0 = y_dev ? yi.dev : (x_dev ? xi.dev : current_device());
+    const bool y_tight = ldy == m_a && ldy2 == m_a * m_b && ldyp == m_a * m_b * m_c;
+    StageSpec sp{ldxp, fpx, ldyp, fpy, beta != T(0) || !y_tight, !scale_only, sizeof(T)};
+    cudaStream_t us = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
+    const bool sync = !(exec && (exec->flags & KB_EXEC_ASYNC) && x_dev && y_dev);
+    const i64 fa = fp_matrix(ac, lda), fb = fp_matrix(bc, ldb), fc = fp_matrix(cc, ldc);
+    auto slice = [&](int dev, i64 p0, i64 p1) {
+      const T *Ad = nullptr, *Bd = nullptr, *Cd = nullptr;
+      run_slice(dev, X, Y, p0, p1, sp, x_dev && xi.dev == dev, y_dev && yi.dev == dev, us, sync,
+                [&](DevRes& r, cudaStream_t s) {
+                  if (scale_only) return;  // A, B, C never read (kron3.hpp:113-128)
+                  T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + fb + fc + 96)));
+                  Ad = const_on_device(A, fa, r.device, cs, s);
+                  Bd = const_on_device(B, fb, r.device, cs + fa + 32, s);
+                  Cd = const_on_device(Cm, fc, r.device, cs + fa + fb + 64, s);
+                },
+                [&](const void* xd, void* yd, i64 n, DevRes& r, cudaStream_t s, int slot) {
+                  if (scale_only) {
+                    const int mode = base.beta_mode;
+                    const int grid = (int)std::max<i64>(
+                        1, std::min<i64>((n * m_a * m_b * m_c + 255) / 256, (i64)r.sm_count * 16));
+                    cuda_check(kb::launch_scale<T>(static_cast<T*>(yd), n, m_a, m_b, m_c, ldy, ldy2, ldyp, mode, beta,
+                                                   grid, s),
+                               "kron3");
+                    count_launch("scale");
+                    return;
+                  }
+                  Kron3Params<T> p = base;
+                  p.A = Ad;
+                  p.B = Bd;
+                  p.C = Cd;
+                  p.X = static_cast<const T*>(xd);
+                  p.Y = static_cast<T*>(yd);
+                  p.batch = n;
+                  cudaError_t e = kb::launch_kron3_fast<T>(p, r.sm_count, s);
+                  if (e == cudaSuccess) {
+                    count_launch("kron3_fast");
+                    return;
+                  }
+                  if (e != cudaErrorNotSupported) cuda_check(e, "kron3");
+                  cudaGetLastError();
+                  const int grid = (int)std::min<i64>(n, (i64)r.sm_count * 8);
+                  const i64 per = m_a * n_b + m_a * m_b * n_c;
+                  T* scratch = nullptr;
+                  i64 scratch_elems = 0;
+                  if ((size_t)per * sizeof(T) > 48 * 1024) {
+                    scratch_elems = per * grid;
+                    scratch = static_cast<T*>(r.scratch[slot].get(sizeof(T) * (size_t)scratch_elems));
+                  }
+                  cuda_check(kb::launch_kron3_generic<T>(p, scratch, scratch_elems, grid, s), "kron3");
+                  count_launch("kron3_generic");
+                });
+    };
+    if (x_dev || y_dev)
+      slice(dev0, 0, batch);
+    else
+      shard(exec, dev0, batch, slice);
+    return KB_OK;
+  } catch (const Fail& f) {
+    return report(f, err, errlen);
+  } catch (const std::exception& e) {
+    return report(Fail{KB_EINTERNAL, std::string("kron3: ") + e.what()}, err, errlen);
+  }
+}
+
+}  // namespace
+
+// =============================================================== C ABI ====
+
+extern "C" {
+
+int kb_skron2(char transa, char transb, char transx, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+              int64_t batch_count, float alpha, const float* A, int64_t lda, int64_t lena, const float* B,
+              int64_t ldb, int64_t lenb, const float* X, int64_t ldx, int64_t ldxp, int64_t lenx, float beta,
+              float* Y, int64_t ldy, int64_t ldyp, int64_t leny, const kb_exec* exec, char* err, size_t errlen) {
+  return kron2_entry<float>(transa, transb, transx, m_a, n_a, m_b, n_b, batch_count, alpha, A, lda, lena, B, ldb,
+                            lenb, X, ldx, ldxp, lenx, beta, Y, ldy, ldyp, leny, exec, err, errlen);
+}
+
+int kb_dkron2(char transa, char transb, char transx, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+              int64_t batch_count, double alpha, const double* A, int64_t lda, int64_t lena, const double* B,
+              int64_t ldb, int64_t lenb, const double* X, int64_t ldx, int64_t ldxp, int64_t lenx, double beta,
+              double* Y, int64_t ldy, int64_t ldyp, int64_t leny, const kb_exec* exec, char* err, size_t errlen) {
+  return kron2_entry<double>(transa, transb, transx, m_a, n_a, m_b, n_b, batch_count, alpha, A, lda, lena, B, ldb,
+                             lenb, X, ldx, ldxp, lenx, beta, Y, ldy, ldyp, leny, exec, err, errlen);
+}
+
+int kb_skron3(char transa, char transb, char transc, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+              int64_t m_c, int64_t n_c, int64_t batch_count, float alpha, const float* A, int64_t lda,
+              int64_t lena, const float* B, int64_t ldb, int64_t lenb, const float* C, int64_t ldc, int64_t lenc,
+              const float* X, int64_t ldx, int64_t ldx2, int64_t ldxp, int64_t lenx, float beta, float* Y,
+              int64_t ldy, int64_t ldy2, int64_t ldyp, int64_t leny, float* work, int64_t work_capacity,
+              const kb_exec* exec, char* err, size_t errlen) {
+  return kron3_entry<float>(transa, transb, transc, m_a, n_a, m_b, n_b, m_c, n_c, batch_count, alpha, A, lda, lena,
+                            B, ldb, lenb, C, ldc, lenc, X, ldx, ldx2, ldxp, lenx, beta, Y, ldy, ldy2, ldyp, leny,
+                            work, work_capacity, exec, err, errlen);
+}
+
+int kb_dkron3(char transa, char transb, char transc, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+              int64_t m_c, int64_t n_c, int64_t batch_count, double alpha, const double* A, int64_t lda,
+              int64_t lena, const double* B, int64_t ldb, int64_t lenb, const double* C, int64_t ldc,
+              int64_t lenc, const double* X, int64_t ldx, int64_t ldx2, int64_t ldxp, int64_t lenx, double beta,
+              double* Y, int64_t ldy, int64_t ldy2, int64_t ldyp, int64_t leny, double* work,
+              int64_t work_capacity, const kb_exec* exec, char* err, size_t errlen) {
+  return kron3_entry<double>(transa, transb, transc, m_a, n_a, m_b, n_b, m_c, n_c, batch_count, alpha, A, lda,
+                             lena, B, ldb, lenb, C, ldc, lenc, X, ldx, ldx2, ldxp, lenx, beta, Y, ldy, ldy2, ldyp,
+                             leny, work, work_capacity, exec, err, errlen);
+}
+
+int kb_kron3_workspace_size(int64_t m_a, int64_t m_b, int64_t n_c, int64_t batch_count, int64_t* out, char* err,
+                            size_t errlen) {
+  // kron3.hpp:43-53
+  if (m_a < 0 || m_b < 0 || n_c < 0 || batch_count < 0)
+    return report(Fail{KB_EINVAL, "kron3_workspace_size: negative dimension"}, err, errlen);
+  int64_t r = m_a;
+  for (int64_t f : {m_b, n_c, batch_count})
+    if (__builtin_mul_overflow(r, f, &r))
+      return report(Fail{KB_EOVERFLOW, "kron3_workspace_size: m_a*m_b*n_c*batch_count overflows"}, err, errlen);
+  if (out) *out = r;
+  return KB_OK;
+}
+
+const char* kb_version(void) { return "kronbatch-b200 0.1 (sm_100a)"; }
+
+uint64_t kb_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char* kb_last_path(void) { return t_last_path.c_str(); }
+
+void kb_release_buffers(void) {
+  for (auto& kv : t_res.by_dev) {
+    DevRes* r = kv.second;
+    DeviceGuard g(r->device);
+    cudaDeviceSynchronize();
+    r->consts.release();
+    for (int i = 0; i < kSlots; ++i) {
+      r->scratch[i].release();
+      r->xs[i].release();
+      r->ys[i].release();
+      cudaStreamDestroy(r->slot_stream[i]);
+    }
+    cudaStreamDestroy(r->stream);
+    delete r;
+  }
+  t_res.by_dev.clear();
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+"""Quick device-resident timing of the fast kernels (development aid, not the bench contract)."""
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+import paper_1304_7054_b200 as kb  # noqa: E402
+from paper_1304_7054_b200 import Array3View, BatchView, KronProblem2D, KronProblem3D, MatrixView, Workspace  # noqa
+
+
+def bench(dims3, n, batch, dtype, reps=10):
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    es = 4 if dtype == "f32" else 8
+    e = n ** (3 if dims3 else 2)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    X = torch.rand(e * batch, dtype=tdt, device="cuda", generator=g) * 2 - 1
+    Y = torch.empty(e * batch, dtype=tdt, device="cuda")
+    A, B, C = (torch.rand(n * n, dtype=tdt, device="cuda", generator=g) * 2 - 1 for _ in range(3))
+    s = torch.cuda.Stream()
+    ex = kb.Exec(stream=s, asynchronous=True)
+    if dims3:
+        pr = KronProblem3D(m_a=n, n_a=n, m_b=n, n_b=n, m_c=n, n_c=n)
+        args = (pr, MatrixView(A, n, n, n), MatrixView(B, n, n, n), MatrixView(C, n, n, n),
+                BatchView(Array3View(X, n, n, n, n, n * n), batch, e), BatchView(Array3View(Y, n, n, n, n, n * n), batch, e),
+                Workspace(None, e * batch))
+        fn = kb.kron3
+    else:
+        pr = KronProblem2D(m_a=n, n_a=n, m_b=n, n_b=n)
+        args = (pr, MatrixView(A, n, n, n), MatrixView(B, n, n, n), BatchView(MatrixView(X, n, n, n), batch, e),
+                BatchView(MatrixView(Y, n, n, n), batch, e))
+        fn = kb.kron2
+    for _ in range(3):
+        fn(*args, exec_=ex)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in evs:
+        a.record(s)
+        fn(*args, exec_=ex)
+        b.record(s)
+    torch.cuda.synchronize()
+    ts = sorted(a.elapsed_time(b) for a, b in evs)
+    ms = ts[len(ts) // 2]
+    flops = (6 * n ** 4 if dims3 else 4 * n ** 3) * batch
+    byts = 2 * e * es * batch
+    print(f"{'3d' if dims3 else '2d'} {dtype} n={n:2d} batch={batch:8d} path={kb.last_path():14s} "
+          f"{ms:8.3f} ms  {flops / ms / 1e9:8.1f} TF/s  {byts / ms / 1e6:7.1f} GB/s  (min {ts[0]:.3f})", flush=True)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1] if len(sys.argv) > 1 else "main"
+    if which == "main":
+        bench(False, 16, 4194304, "f32")
+        bench(False, 10, 65536 * 16, "f32")
+        bench(True, 16, 262144, "f32")
+        bench(True, 10, 262144, "f32")
+        bench(True, 16, 131072, "f64")
+        bench(False, 16, 2097152, "f64")
+    elif which == "one":  # one <2|3> <n> <f32|f64> <batch> [reps]
+        reps = int(sys.argv[6]) if len(sys.argv) > 6 else 3
+        bench(sys.argv[2] == "3", int(sys.argv[3]), int(sys.argv[5]), sys.argv[4], reps=reps)
+    else:
+        for dims3 in (False, True):
+            for dt in ("f32", "f64"):
+                for n in range(1, 17):
+                    es = 4 if dt == "f32" else 8
+                    e = n ** (3 if dims3 else 2)
+                    batch = max(1, int(2 * 1024 ** 3 // (e * es)))
+                    bench(dims3, n, batch, dt, reps=5)
