@@ -121,15 +121,19 @@ __device__ __forceinline__ void stage_rows(T* w, const T* M, long long ldm, int 
 }
 
 // ------------------------------------------------------------- contraction --
+// All loops below are fully unrolled; operands are fetched from smem in
+// vector chunks right before use so that only the accumulators stay live.
+// Each accumulator receives its terms in ascending contraction index.
 
 // tmp(I_q, m) = sum_l A_r(I_q, l) Xop(l, m) for all m, from one smem plane.
-// OPX = 0: plane holds Xop column-major (column m contiguous); m-outer.
-// OPX = 1: plane holds X stored (= Xop^T), i.e. row l of Xop contiguous; l-outer.
+// OPX = 0: plane holds Xop column-major (column m contiguous): m-blocks of MB
+//          columns, l in chunks of VXR (MB * R/2 independent FFMA2 chains).
+// OPX = 1: plane holds X as stored (= Xop^T): row l of Xop contiguous; l-outer.
 template <typename T, int N, int OPX, int MB>
 __device__ __forceinline__ void mode1(T (&t)[N][SqCfg<T, N>::R], const T* __restrict__ xs,
                                       const T* __restrict__ aq) {
   using C = SqCfg<T, N>;
-  constexpr int R = C::R;
+  constexpr int R = C::R, LC = C::VXR;
 #pragma unroll
   for (int m = 0; m < N; ++m)
 #pragma unroll
@@ -137,17 +141,20 @@ __device__ __forceinline__ void mode1(T (&t)[N][SqCfg<T, N>::R], const T* __rest
   if constexpr (OPX == 0) {
 #pragma unroll
     for (int m0 = 0; m0 < N; m0 += MB) {
-      T xc[MB][N];
 #pragma unroll
-      for (int mm = 0; mm < MB; ++mm)
-        if (m0 + mm < N) lds_n<N, C::VXR>(xc[mm], xs + (m0 + mm) * N);
-#pragma unroll
-      for (int l = 0; l < N; ++l) {
-        T a[R];
-        lds_n<R, C::VR>(a, aq + l * R);
+      for (int l0 = 0; l0 < N; l0 += LC) {
+        T xc[MB][LC];
+        T a[LC][R];
 #pragma unroll
         for (int mm = 0; mm < MB; ++mm)
-          if (m0 + mm < N) axpy_rows<R>(t[m0 + mm], a, xc[mm][l]);
+          if (m0 + mm < N) lds_vec<LC>(xc[mm], xs + (m0 + mm) * N + l0);
+#pragma unroll
+        for (int ll = 0; ll < LC; ++ll) lds_n<R, C::VR>(a[ll], aq + (l0 + ll) * R);
+#pragma unroll
+        for (int ll = 0; ll < LC; ++ll)
+#pragma unroll
+          for (int mm = 0; mm < MB; ++mm)
+            if (m0 + mm < N) axpy_rows<R>(t[m0 + mm], a[ll], xc[mm][ll]);
       }
     }
   } else {
@@ -163,19 +170,77 @@ __device__ __forceinline__ void mode1(T (&t)[N][SqCfg<T, N>::R], const T* __rest
   }
 }
 
+// out[jj] (+)= sum_m t[m] * w(j0+jj, m) for jj < JB, m ascending; w rows
+// contiguous in smem (broadcast reads), fetched VN elements at a time.
+template <typename T, int N, int JB>
+__device__ __forceinline__ void contract_rows(T (&out)[JB][SqCfg<T, N>::R], const T (&t)[N][SqCfg<T, N>::R],
+                                              const T* __restrict__ wrow, int j0) {
+  using C = SqCfg<T, N>;
+  constexpr int R = C::R, VN = C::VN;
+#pragma unroll
+  for (int m0 = 0; m0 < N; m0 += VN) {
+    T wv[JB][VN];
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj)
+      if (j0 + jj < N) lds_vec<VN>(wv[jj], wrow + (j0 + jj) * N + m0);
+#pragma unroll
+    for (int mm = 0; mm < VN; ++mm)
+#pragma unroll
+      for (int jj = 0; jj < JB; ++jj)
+        if (j0 + jj < N) axpy_rows<R>(out[jj], t[m0 + mm], wv[jj][mm]);
+  }
+}
+
+// Y(I_q, j) block init from beta (detail.hpp:45-51), reading the prior only when needed.
+template <typename T, int N>
+__device__ __forceinline__ void init_y(T (&y)[SqCfg<T, N>::R], const T* yc, int rows, int beta_mode, T beta) {
+  using C = SqCfg<T, N>;
+  constexpr int R = C::R;
+  if (beta_mode == kBetaZero) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) y[r] = T(0);
+    return;
+  }
+  if (R * C::TPI == N || rows >= R) {
+    ldg_n<R, C::VY>(y, yc);
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r) y[r] = r < rows ? yc[r] : T(0);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) y[r] = beta_init(beta_mode, beta, y[r]);
+}
+
+template <typename T, int N>
+__device__ __forceinline__ void store_y(T* yc, const T (&y)[SqCfg<T, N>::R], int rows) {
+  using C = SqCfg<T, N>;
+  constexpr int R = C::R;
+  if (R * C::TPI == N || rows >= R) {
+    stg_n<R, C::VY>(yc, y);
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (r < rows) yc[r] = y[r];
+  }
+}
+
 // ---------------------------------------------------------------- kron2 ---
 
 // Launch/tiling policy; V selects a tuning variant (V = 0 is the default).
 template <typename T, int N, int V = 0>
 struct Kron2Fast {
   using C = SqCfg<T, N>;
-  static constexpr int WARPS = V == 2 ? 4 : (V == 3 ? 12 : 8);
-  static constexpr int STAGES = V == 2 ? 4 : (V == 3 ? 2 : 3);
-  static constexpr int MB = V == 1 ? 2 : 4;  // X columns held per mode-1 block
-  static constexpr int JB = V == 3 ? 4 : 2;  // Y columns per mode-2 block
+  static constexpr bool F32 = sizeof(T) == 4;
+  static constexpr int WARPS = V == 0 ? 12 : (V == 1 ? 8 : (V == 2 ? 16 : 12));
+  static constexpr int STAGES = V == 0 ? 2 : (V == 1 ? 3 : (V == 2 ? 1 : 2));
+  static constexpr int MB = V == 3 ? 2 : 4;  // X columns per mode-1 block
+  static constexpr int JB = V == 3 ? 2 : 4;  // Y columns per mode-2 block
+  // whole entries are 16-byte multiples: one cp.async.bulk per entry
+  static constexpr bool BULK = (C::NN * sizeof(T)) % 16 == 0;
   static constexpr int RING = C::IPW * C::SLOT;  // elements per warp stage
   static constexpr size_t smem_bytes() {
-    return sizeof(T) * ((size_t)C::A_ELEMS + (size_t)C::ROW_ELEMS + (size_t)WARPS * STAGES * RING);
+    return sizeof(T) * ((size_t)C::A_ELEMS + (size_t)C::ROW_ELEMS + (size_t)WARPS * STAGES * RING) +
+           sizeof(unsigned long long) * WARPS * STAGES;
   }
 };
 
@@ -184,220 +249,290 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
     kron2_sq_kernel(const Kron2Params<T> p, const long long ngroups) {
   using K = Kron2Fast<T, N, V>;
   using C = SqCfg<T, N>;
-  constexpr int R = C::R, TPI = C::TPI, IPW = C::IPW, NN = C::NN, VXC = C::VXC;
+  constexpr int R = C::R, TPI = C::TPI, IPW = C::IPW, NN = C::NN, VXC = C::VXC, S = K::STAGES;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* ablk = reinterpret_cast<T*>(smem_raw);
   T* wrow = ablk + C::A_ELEMS;
   T* ring = wrow + C::ROW_ELEMS;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(ring + K::WARPS * S * K::RING);
 
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if constexpr (K::BULK) {
+    if (lane == 0)
+      for (int s = 0; s < S; ++s) mbar_init(&bars[warp * S + s], 1);
+    mbar_fence_init();
+  }
   stage_a<T, N>(ablk, p.A, p.lda, p.opa);
   stage_rows<T, N>(wrow, p.B, p.ldb, p.opb, p.alpha, true);
   __syncthreads();
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  T* wring = ring + warp * K::STAGES * K::RING;
+  T* wring = ring + warp * S * K::RING;
+  unsigned long long* wbar = bars + warp * S;
   const long long gw = (long long)blockIdx.x * K::WARPS + warp;
   const long long gstride = (long long)gridDim.x * K::WARPS;
 
-  // cp.async one group of IPW entries into a stage (zero-fill past the batch)
+  // start loading group g (IPW entries) into `stage`
   auto issue = [&](long long g, int stage) {
-    if (g < ngroups) {
-      T* dst = wring + stage * K::RING;
+    if (g >= ngroups) {
+      if constexpr (!K::BULK) cp_async_commit();
+      return;
+    }
+    T* dst = wring + stage * K::RING;
+    const long long first = g * IPW;
+    const int valid = (int)(p.batch - first < IPW ? p.batch - first : IPW);
+    if constexpr (K::BULK) {
+      if (lane == 0) mbar_arrive_expect_tx(&wbar[stage], (unsigned)(valid * NN * sizeof(T)));
+      __syncwarp();
+      if (lane < valid) bulk_g2s(dst + lane * C::SLOT, p.X + (first + lane) * p.sx, NN * sizeof(T), &wbar[stage]);
+    } else {
       constexpr int CPI = NN / VXC;  // chunks per entry
+#pragma unroll 4
       for (int c = lane; c < IPW * CPI; c += 32) {
-        const int e = c / CPI, r = c % CPI;
-        const long long item = g * IPW + e;
-        const bool ok = item < p.batch;
-        const T* src = p.X + (ok ? item : 0) * p.sx + r * VXC;
+        const int e = c / CPI, r = c - e * CPI;
+        const bool ok = e < valid;
+        const T* src = p.X + (first + (ok ? e : 0)) * p.sx + r * VXC;
         cp_async<VXC * sizeof(T)>(dst + e * C::SLOT + r * VXC, src, ok);
       }
+      cp_async_commit();
     }
-    cp_async_commit();
   };
 
 #pragma unroll
-  for (int s = 0; s < K::STAGES - 1; ++s) issue(gw + s * gstride, s);
+  for (int s = 0; s < S - 1; ++s) issue(gw + s * gstride, s);
 
   const int slot = lane / TPI, q = lane % TPI;
   const T* aq = ablk + q * C::QS;
+  const int rows = N - q * R;  // valid rows of this block (>= R unless padded)
   int stage = 0;
+  unsigned phase = 0;  // parity of the current use of `stage`
   for (long long g = gw; g < ngroups; g += gstride) {
-    issue(g + (K::STAGES - 1) * gstride, (stage + K::STAGES - 1) % K::STAGES);
-    cp_async_wait<K::STAGES - 1>();
-    __syncwarp();
+    issue(g + (S - 1) * gstride, (stage + S - 1) % S);
+    if constexpr (K::BULK) {
+      mbar_wait(&wbar[stage], phase);
+    } else {
+      cp_async_wait<S - 1>();
+      __syncwarp();
+    }
     const long long item = g * IPW + slot;
-    if (slot < IPW && item < p.batch) {
+    if (item < p.batch) {
       const T* xs = wring + stage * K::RING + slot * C::SLOT;
       T t[N][R];
       mode1<T, N, OPX, K::MB>(t, xs, aq);
       T* yb = p.Y + item * p.sy + q * R;
-      const int rows = N - q * R;  // valid rows of this block (>= R unless padded)
 #pragma unroll
       for (int j0 = 0; j0 < N; j0 += K::JB) {
-        T w[K::JB][N];
         T y[K::JB][R];
 #pragma unroll
-        for (int jj = 0; jj < K::JB; ++jj) {
-          if (j0 + jj < N) {
-            lds_n<N, C::VN>(w[jj], wrow + (j0 + jj) * N);
-            if (p.beta_mode == kBetaZero) {
+        for (int jj = 0; jj < K::JB; ++jj)
+          if (j0 + jj < N) init_y<T, N>(y[jj], yb + (long long)(j0 + jj) * p.ldy, rows, p.beta_mode, p.beta);
+        contract_rows<T, N, K::JB>(y, t, wrow, j0);
 #pragma unroll
-              for (int r = 0; r < R; ++r) y[jj][r] = T(0);
-            } else {
-              T* yc = yb + (long long)(j0 + jj) * p.ldy;
-              if (R * TPI == N || rows >= R) {
-                ldg_n<R, C::VY>(y[jj], yc);
-              } else {
-#pragma unroll
-                for (int r = 0; r < R; ++r) y[jj][r] = r < rows ? yc[r] : T(0);
-              }
-#pragma unroll
-              for (int r = 0; r < R; ++r) y[jj][r] = beta_init(p.beta_mode, p.beta, y[jj][r]);
-            }
-          }
-        }
-#pragma unroll
-        for (int m = 0; m < N; ++m)
-#pragma unroll
-          for (int jj = 0; jj < K::JB; ++jj)
-            if (j0 + jj < N) axpy_rows<R>(y[jj], t[m], w[jj][m]);
-#pragma unroll
-        for (int jj = 0; jj < K::JB; ++jj) {
-          if (j0 + jj < N) {
-            T* yc = yb + (long long)(j0 + jj) * p.ldy;
-            if (R * TPI == N || rows >= R) {
-              stg_n<R, C::VY>(yc, y[jj]);
-            } else {
-#pragma unroll
-              for (int r = 0; r < R; ++r)
-                if (r < rows) yc[r] = y[jj][r];
-            }
-          }
-        }
+        for (int jj = 0; jj < K::JB; ++jj)
+          if (j0 + jj < N) store_y<T, N>(yb + (long long)(j0 + jj) * p.ldy, y[jj], rows);
       }
     }
-    __syncwarp();
-    stage = (stage + 1) % K::STAGES;
+    __syncwarp();  // the stage is refilled by the next issue()
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1;
+    }
   }
-  cp_async_wait<0>();
+  if constexpr (!K::BULK) cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------- kron3 ---
 
+// Worst bank multiplicity of one LDS/STS phase in which lane k accesses
+// `width` elements at (k / tpi) * stride + (k % tpi) * r (equal addresses broadcast).
+__host__ __device__ constexpr int phase_conflicts(int stride, int tpi, int r, int width, int es) {
+  const int lanes = 128 / (width * es) < 32 ? 128 / (width * es) : 32;
+  int cnt[32] = {};
+  int worst = 0;
+  const int wb = width * es / 4 > 0 ? width * es / 4 : 1;
+  for (int k = 0; k < lanes; ++k) {
+    const long long off = (long long)(k / tpi) * stride + (long long)(k % tpi) * r;
+    bool dup = false;
+    for (int k2 = 0; k2 < k && !dup; ++k2) dup = (long long)(k2 / tpi) * stride + (long long)(k2 % tpi) * r == off;
+    if (dup) continue;
+    for (int b = 0; b < wb; ++b) {
+      const int bank = (int)((off * es / 4 + b) % 32);
+      if (++cnt[bank] > worst) worst = cnt[bank];
+    }
+  }
+  return worst;
+}
+
+// 3-D plane stride: conflict-free mode-1 column reads (planes of a phase at
+// k*stride, TPI lanes broadcasting) AND conflict-free T2 row-block writes
+// (lane (s, q) at s*stride + q*R); a multiple of 16 bytes for bulk copies.
+template <typename T, int N>
+__host__ __device__ constexpr int plane_stride3() {
+  using C = SqCfg<T, N>;
+  const int es = sizeof(T);
+  int align = C::VXC > C::VXR ? C::VXC : C::VXR;
+  if ((C::NN * es) % 16 == 0) align = 16 / es;
+  const int first = ((C::NN + align - 1) / align) * align;
+  int best = first, best_c = 1 << 30;
+  for (int s = first; s <= first + 64 * align; s += align) {
+    if (s % C::VR) continue;
+    const int cr = phase_conflicts(s, C::TPI, 0, C::VXR, es);
+    const int cw = C::PLANE_VEC ? phase_conflicts(s, C::TPI, C::R, C::VR, es) : 1;
+    const int c = cr > cw ? cr : cw;
+    if (c < best_c) {
+      best_c = c;
+      best = s;
+      if (c == 1) break;
+    }
+  }
+  return best;
+}
+
 template <typename T, int N, int V = 0>
 struct Kron3Fast {
   using C = SqCfg<T, N>;
-  static constexpr int PT = N * C::TPI;  // threads per entry
-  static constexpr int MAXT = V == 0 ? 256 : (V == 3 ? 64 : 128);
+  static constexpr int PT = N * C::TPI;  // threads per entry (one plane task + one fiber block each)
+  static constexpr int MAXT = V == 1 ? 256 : (V == 2 ? 64 : 128);
   static constexpr int IT = (MAXT / PT) > 0 ? MAXT / PT : 1;  // entries per tile
   static constexpr int THREADS = IT * PT;
-  static constexpr int STAGES = 2;
-  static constexpr int MB = (V == 2 || V == 3) ? 2 : 4;
-  static constexpr int JB = 2;
-  static constexpr int KB = 2;
-  static constexpr int ITEM = N * C::SLOT;  // padded entry stride (planes at SLOT)
+  static constexpr int STAGES = V == 3 ? 1 : 2;
+  static constexpr int MINB = V == 1 ? 1 : (V == 2 ? 6 : (V == 3 ? 4 : 3));  // resident CTAs/SM targeted
+  static constexpr int MB = 4;
+  static constexpr int JB = sizeof(T) == 4 ? 4 : 4;
+  static constexpr int KB = JB;
+  static constexpr bool BULK = (C::NN * sizeof(T)) % 16 == 0;  // one cp.async.bulk per plane
+  static constexpr int PS = plane_stride3<T, N>();             // plane stride in smem
+  static constexpr int ITEM = N * PS;                          // entry stride in smem
   static constexpr int TILE = IT * ITEM;
   static constexpr size_t smem_bytes() {
-    return sizeof(T) * ((size_t)C::A_ELEMS + 2 * (size_t)C::ROW_ELEMS + (size_t)STAGES * TILE);
+    return sizeof(T) * ((size_t)C::A_ELEMS + 2 * (size_t)C::ROW_ELEMS + (size_t)STAGES * TILE) +
+           sizeof(unsigned long long) * STAGES;
   }
 };
 
+// Store R rows (the valid prefix when the block is padded) to smem.
+template <typename T, int N>
+__device__ __forceinline__ void sts_rows(T* dst, const T (&v)[SqCfg<T, N>::R], int rows) {
+  using C = SqCfg<T, N>;
+  constexpr int R = C::R;
+  if (R * C::TPI == N || rows >= R) {
+    if constexpr (C::PLANE_VEC) {
+#pragma unroll
+      for (int r = 0; r < R; r += C::VR) {
+        if constexpr (C::VR * sizeof(T) == 16 && sizeof(T) == 4)
+          *reinterpret_cast<float4*>(dst + r) = make_float4(v[r], v[r + 1], v[r + 2], v[r + 3]);
+        else if constexpr (C::VR * sizeof(T) == 16)
+          *reinterpret_cast<double2*>(dst + r) = make_double2(v[r], v[r + 1]);
+        else if constexpr (C::VR == 2 && sizeof(T) == 4)
+          *reinterpret_cast<float2*>(dst + r) = make_float2(v[r], v[r + 1]);
+        else
+          dst[r] = v[r];
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[r] = v[r];
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (r < rows) dst[r] = v[r];
+  }
+}
+
 template <typename T, int N, int V>
-__global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS)
+__global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS, Kron3Fast<T, N, V>::MINB)
     kron3_sq_kernel(const Kron3Params<T> p, const long long ntiles) {
   using K = Kron3Fast<T, N, V>;
   using C = SqCfg<T, N>;
-  constexpr int R = C::R, TPI = C::TPI, NN = C::NN, VXC = C::VXC, IT = K::IT;
+  constexpr int R = C::R, TPI = C::TPI, NN = C::NN, VXC = C::VXC, IT = K::IT, PS = K::PS, S = K::STAGES;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* ablk = reinterpret_cast<T*>(smem_raw);
-  T* brow = ablk + C::A_ELEMS;  // B_r rows (stage 1b: alpha 1, exact)
-  T* crow = brow + C::ROW_ELEMS;        // fl(alpha*C_r) rows
+  T* brow = ablk + C::A_ELEMS;     // B_r rows (stage 1b: alpha 1, exact)
+  T* crow = brow + C::ROW_ELEMS;   // fl(alpha*C_r) rows
   T* tiles = crow + C::ROW_ELEMS;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(tiles + S * K::TILE);
 
+  const int tid = threadIdx.x;
+  if constexpr (K::BULK) {
+    if (tid == 0)
+      for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+  }
   stage_a<T, N>(ablk, p.A, p.lda, p.opa);
   stage_rows<T, N>(brow, p.B, p.ldb, p.opb, T(1), false);
   stage_rows<T, N>(crow, p.C, p.ldc, p.opc, p.alpha, true);
   __syncthreads();
 
-  const int tid = threadIdx.x;
+  // start loading tile `tile` (IT entries, N planes each) into `stage`; warp 0 issues
   auto issue = [&](long long tile, int stage) {
-    if (tile < ntiles) {
-      T* dst = tiles + stage * K::TILE;
-      constexpr int CPP = NN / VXC;       // chunks per plane
-      constexpr int CPE = N * CPP;        // chunks per entry
-      for (int c = tid; c < IT * CPE; c += K::THREADS) {
-        const int e = c / CPE, rr = c % CPE, n = rr / CPP, r = rr % CPP;
-        const long long item = tile * IT + e;
-        const bool ok = item < p.batch;
-        const T* src = p.X + (ok ? item : 0) * p.sx + (long long)n * NN + r * VXC;
-        cp_async<VXC * sizeof(T)>(dst + e * K::ITEM + n * C::SLOT + r * VXC, src, ok);
-      }
+    if (tile >= ntiles) {
+      if constexpr (!K::BULK) cp_async_commit();
+      return;
     }
-    cp_async_commit();
+    T* dst = tiles + stage * K::TILE;
+    const long long first = tile * IT;
+    const int valid = (int)(p.batch - first < IT ? p.batch - first : IT);
+    if constexpr (K::BULK) {
+      if (tid < 32) {
+        if (tid == 0) mbar_arrive_expect_tx(&bars[stage], (unsigned)(valid * N * NN * sizeof(T)));
+        __syncwarp();
+        for (int pl = tid; pl < valid * N; pl += 32) {
+          const int e = pl / N, n = pl - e * N;
+          bulk_g2s(dst + e * K::ITEM + n * PS, p.X + (first + e) * p.sx + (long long)n * NN, NN * sizeof(T),
+                   &bars[stage]);
+        }
+      }
+    } else {
+      constexpr int CPP = NN / VXC;  // chunks per plane
+      constexpr int CPE = N * CPP;   // chunks per entry
+      for (int c = tid; c < IT * CPE; c += K::THREADS) {
+        const int e = c / CPE, rr = c - e * CPE, n = rr / CPP, r = rr - n * CPP;
+        const bool ok = e < valid;
+        const T* src = p.X + (first + (ok ? e : 0)) * p.sx + (long long)n * NN + r * VXC;
+        cp_async<VXC * sizeof(T)>(dst + e * K::ITEM + n * PS + r * VXC, src, ok);
+      }
+      cp_async_commit();
+    }
   };
 
-  issue(blockIdx.x, 0);
   const int task = tid / TPI, q = tid % TPI;  // plane task: entry task/N, plane task%N
   const int te = task / N, tn = task % N;
   const T* aq = ablk + q * C::QS;
-  // mode-3 fiber block: entry fe, column j, rows I_q
-  const int fe = tid / K::PT, fj = (tid % K::PT) / TPI;
+  const int fe = te, fj = tn;  // mode-3 fiber block (entry fe, column j = fj, rows I_q)
+  const int rows = N - q * R;
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) issue(blockIdx.x + (long long)s * gridDim.x, s);
   int stage = 0;
+  unsigned phase = 0;
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    issue(tile + gridDim.x, stage ^ 1);
-    cp_async_wait<1>();
-    __syncthreads();
+    if constexpr (S == 1) {
+      issue(tile, 0);
+    } else {
+      issue(tile + (long long)(S - 1) * gridDim.x, (stage + S - 1) % S);
+    }
+    if constexpr (K::BULK) {
+      mbar_wait(&bars[stage], phase);
+    } else {
+      cp_async_wait<S - 1>();
+      __syncthreads();
+    }
     T* buf = tiles + stage * K::TILE;
-    const int rows = N - q * R;
-    // ---- modes 1 and 2 on plane (te, tn): T2(I_q, :, tn) -> in place
+    // ---- modes 1 and 2 on plane (te, tn); T2(I_q, :, tn) overwrites the X plane
     {
-      T* xs = buf + te * K::ITEM + tn * C::SLOT;
+      T* xs = buf + te * K::ITEM + tn * PS;
       T t[N][R];
       mode1<T, N, 0, K::MB>(t, xs, aq);
-      T t2[N][R];
+      __syncwarp();  // every lane of this warp finished reading its X plane
 #pragma unroll
       for (int j0 = 0; j0 < N; j0 += K::JB) {
-        T w[K::JB][N];
+        T t2[K::JB][R];
 #pragma unroll
         for (int jj = 0; jj < K::JB; ++jj)
-          if (j0 + jj < N) {
-            lds_n<N, C::VN>(w[jj], brow + (j0 + jj) * N);
 #pragma unroll
-            for (int r = 0; r < R; ++r) t2[j0 + jj][r] = T(0);
-          }
+          for (int r = 0; r < R; ++r) t2[jj][r] = T(0);
+        contract_rows<T, N, K::JB>(t2, t, brow, j0);
 #pragma unroll
-        for (int m = 0; m < N; ++m)
-#pragma unroll
-          for (int jj = 0; jj < K::JB; ++jj)
-            if (j0 + jj < N) axpy_rows<R>(t2[j0 + jj], t[m], w[jj][m]);
-      }
-      __syncwarp();  // all TPI threads of this plane finished reading X
-#pragma unroll
-      for (int j = 0; j < N; ++j) {
-        T* dst = xs + j * N + q * R;
-        if (R * TPI == N || rows >= R) {
-          if constexpr (C::PLANE_VEC) {
-            // aligned vector store into smem
-#pragma unroll
-            for (int r = 0; r < R; r += C::VR) {
-              if constexpr (C::VR * sizeof(T) == 16 && sizeof(T) == 4)
-                *reinterpret_cast<float4*>(dst + r) = make_float4(t2[j][r], t2[j][r + 1], t2[j][r + 2], t2[j][r + 3]);
-              else if constexpr (C::VR * sizeof(T) == 16)
-                *reinterpret_cast<double2*>(dst + r) = make_double2(t2[j][r], t2[j][r + 1]);
-              else if constexpr (C::VR == 2 && sizeof(T) == 4)
-                *reinterpret_cast<float2*>(dst + r) = make_float2(t2[j][r], t2[j][r + 1]);
-              else
-                dst[r] = t2[j][r];
-            }
-          } else {
-#pragma unroll
-            for (int r = 0; r < R; ++r) dst[r] = t2[j][r];
-          }
-        } else {
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-            if (r < rows) dst[r] = t2[j][r];
-        }
+        for (int jj = 0; jj < K::JB; ++jj)
+          if (j0 + jj < N) sts_rows<T, N>(xs + (j0 + jj) * N + q * R, t2[jj], rows);
       }
     }
     __syncthreads();
@@ -411,66 +546,38 @@ __global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS)
         for (int n = 0; n < N; ++n) {
           if (R * TPI == N || rows >= R) {
             if constexpr (C::PLANE_VEC)
-              lds_n<R, C::VR>(f[n], fb + n * C::SLOT);
+              lds_n<R, C::VR>(f[n], fb + n * PS);
             else {
 #pragma unroll
-              for (int r = 0; r < R; ++r) f[n][r] = fb[n * C::SLOT + r];
+              for (int r = 0; r < R; ++r) f[n][r] = fb[n * PS + r];
             }
           } else {
 #pragma unroll
-            for (int r = 0; r < R; ++r) f[n][r] = r < rows ? fb[n * C::SLOT + r] : T(0);
+            for (int r = 0; r < R; ++r) f[n][r] = r < rows ? fb[n * PS + r] : T(0);
           }
         }
         T* yb = p.Y + item * p.sy + (long long)fj * p.ldy + q * R;
 #pragma unroll
         for (int k0 = 0; k0 < N; k0 += K::KB) {
-          T w[K::KB][N];
           T y[K::KB][R];
 #pragma unroll
-          for (int kk = 0; kk < K::KB; ++kk) {
-            if (k0 + kk < N) {
-              lds_n<N, C::VN>(w[kk], crow + (k0 + kk) * N);
-              if (p.beta_mode == kBetaZero) {
+          for (int kk = 0; kk < K::KB; ++kk)
+            if (k0 + kk < N) init_y<T, N>(y[kk], yb + (long long)(k0 + kk) * p.ldy2, rows, p.beta_mode, p.beta);
+          contract_rows<T, N, K::KB>(y, f, crow, k0);
 #pragma unroll
-                for (int r = 0; r < R; ++r) y[kk][r] = T(0);
-              } else {
-                const T* yc = yb + (long long)(k0 + kk) * p.ldy2;
-                if (R * TPI == N || rows >= R) {
-                  ldg_n<R, C::VY>(y[kk], yc);
-                } else {
-#pragma unroll
-                  for (int r = 0; r < R; ++r) y[kk][r] = r < rows ? yc[r] : T(0);
-                }
-#pragma unroll
-                for (int r = 0; r < R; ++r) y[kk][r] = beta_init(p.beta_mode, p.beta, y[kk][r]);
-              }
-            }
-          }
-#pragma unroll
-          for (int n = 0; n < N; ++n)
-#pragma unroll
-            for (int kk = 0; kk < K::KB; ++kk)
-              if (k0 + kk < N) axpy_rows<R>(y[kk], f[n], w[kk][n]);
-#pragma unroll
-          for (int kk = 0; kk < K::KB; ++kk) {
-            if (k0 + kk < N) {
-              T* yc = yb + (long long)(k0 + kk) * p.ldy2;
-              if (R * TPI == N || rows >= R) {
-                stg_n<R, C::VY>(yc, y[kk]);
-              } else {
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-                  if (r < rows) yc[r] = y[kk][r];
-              }
-            }
-          }
+          for (int kk = 0; kk < K::KB; ++kk)
+            if (k0 + kk < N) store_y<T, N>(yb + (long long)(k0 + kk) * p.ldy2, y[kk], rows);
         }
       }
     }
+    if constexpr (K::BULK) fence_proxy_async();  // generic T2 writes before the next TMA refill
     __syncthreads();
-    stage ^= 1;
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1;
+    }
   }
-  cp_async_wait<0>();
+  if constexpr (!K::BULK) cp_async_wait<0>();
 }
 
 }  // namespace kb

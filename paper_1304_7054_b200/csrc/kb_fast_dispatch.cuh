@@ -53,6 +53,7 @@ static cudaError_t launch2v(const Kron2Params<T>& p, int sm_count, cudaStream_t 
   using C = SqCfg<T, N>;
   using K = Kron2Fast<T, N, V>;
   if (p.ldx != N || p.sx % C::VXC || !aligned<T>(p.X, C::VXC)) return cudaErrorNotSupported;
+  if (K::BULK && ((p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))) return cudaErrorNotSupported;
   if (p.ldy % C::VY || p.sy % C::VY || !aligned<T>(p.Y, C::VY)) return cudaErrorNotSupported;
   auto kern = kron2_sq_kernel<T, N, OPX, V>;
   const int threads = K::WARPS * 32;
@@ -86,6 +87,7 @@ static cudaError_t launch3v(const Kron3Params<T>& p, int sm_count, cudaStream_t 
   using K = Kron3Fast<T, N, V>;
   if (p.ldx != N || p.ldx2 != (long long)N * N || p.sx % C::VXC || !aligned<T>(p.X, C::VXC))
     return cudaErrorNotSupported;
+  if (K::BULK && ((p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))) return cudaErrorNotSupported;
   if (p.ldy % C::VY || p.ldy2 % C::VY || p.sy % C::VY || !aligned<T>(p.Y, C::VY)) return cudaErrorNotSupported;
   auto kern = kron3_sq_kernel<T, N, V>;
   const size_t smem = K::smem_bytes();
