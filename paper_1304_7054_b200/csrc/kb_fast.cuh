@@ -97,7 +97,37 @@ struct SqCfg {
   static constexpr int ROW_ELEMS = align16_elems(N * N, ES);
 };
 
+// Op-resolved constant matrices, passed BY VALUE as __grid_constant__ kernel
+// parameters: the broadcast operands of the second/third contractions are read
+// straight from the constant bank into uniform registers (LDCU -> FFMA2 UR
+// operand), so they cost no shared-memory wavefronts and no LDS issue slots.
+//   a[i + l*N] = A_r(i, l)            (staged once into smem per CTA)
+//   w[j*N + m] = fl(alpha * B_r(j, m)) (2-D)
+//   b[j*N + m] = B_r(j, m), c[k*N + n] = fl(alpha * C_r(k, n)) (3-D)
+template <typename T, int N>
+struct SqConsts2 {
+  T a[N * N];
+  T w[N * N];
+};
+template <typename T, int N>
+struct SqConsts3 {
+  T a[N * N];
+  T b[N * N];
+  T c[N * N];
+};
+
 // ------------------------------------------------------- constant staging --
+
+// Ablk[q*QS + l*R + r] = A_r(q*R + r, l) from the resolved parameter copy
+template <typename T, int N>
+__device__ __forceinline__ void stage_a_param(T* ablk, const T (&a)[N * N]) {
+  using C = SqCfg<T, N>;
+  for (int t = threadIdx.x; t < C::TPI * N * C::R; t += blockDim.x) {
+    const int r = t % C::R, l = (t / C::R) % N, q = t / (C::R * N);
+    const int i = q * C::R + r;
+    ablk[q * C::QS + l * C::R + r] = i < N ? a[i + l * N] : T(0);
+  }
+}
 
 // Ablk[q*QS + l*R + r] = A_r(q*R + r, l) (0 for padded rows >= N)
 template <typename T, int N>
@@ -170,6 +200,34 @@ __device__ __forceinline__ void mode1(T (&t)[N][SqCfg<T, N>::R], const T* __rest
   }
 }
 
+// Mode 1 (OPX = 0) with this thread's A rows held in registers: ar[l][r] =
+// A_r(q*R + r, l). Saves the per-m-block A re-reads (smem wavefronts).
+template <typename T, int N, int MB>
+__device__ __forceinline__ void mode1_areg(T (&t)[N][SqCfg<T, N>::R], const T* __restrict__ xs,
+                                           const T (&ar)[N][SqCfg<T, N>::R]) {
+  using C = SqCfg<T, N>;
+  constexpr int R = C::R, LC = C::VXR;
+#pragma unroll
+  for (int m = 0; m < N; ++m)
+#pragma unroll
+    for (int r = 0; r < R; ++r) t[m][r] = T(0);
+#pragma unroll
+  for (int m0 = 0; m0 < N; m0 += MB) {
+#pragma unroll
+    for (int l0 = 0; l0 < N; l0 += LC) {
+      T xc[MB][LC];
+#pragma unroll
+      for (int mm = 0; mm < MB; ++mm)
+        if (m0 + mm < N) lds_vec<LC>(xc[mm], xs + (m0 + mm) * N + l0);
+#pragma unroll
+      for (int ll = 0; ll < LC; ++ll)
+#pragma unroll
+        for (int mm = 0; mm < MB; ++mm)
+          if (m0 + mm < N) axpy_rows<R>(t[m0 + mm], ar[l0 + ll], xc[mm][ll]);
+    }
+  }
+}
+
 // out[jj] (+)= sum_m t[m] * w(j0+jj, m) for jj < JB, m ascending; w rows
 // contiguous in smem (broadcast reads), fetched VN elements at a time.
 template <typename T, int N, int JB>
@@ -189,6 +247,20 @@ __device__ __forceinline__ void contract_rows(T (&out)[JB][SqCfg<T, N>::R], cons
       for (int jj = 0; jj < JB; ++jj)
         if (j0 + jj < N) axpy_rows<R>(out[jj], t[m0 + mm], wv[jj][mm]);
   }
+}
+
+// Same contraction with the w rows read from a __grid_constant__ parameter
+// (compile-time offsets -> constant bank -> uniform registers).
+template <typename T, int N, int JB>
+__device__ __forceinline__ void contract_rows_c(T (&out)[JB][SqCfg<T, N>::R], const T (&t)[N][SqCfg<T, N>::R],
+                                                const T (&w)[N * N], int j0) {
+  using C = SqCfg<T, N>;
+  constexpr int R = C::R;
+#pragma unroll
+  for (int m = 0; m < N; ++m)
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj)
+      if (j0 + jj < N) axpy_rows<R>(out[jj], t[m], w[(j0 + jj) * N + m]);
 }
 
 // Y(I_q, j) block init from beta (detail.hpp:45-51), reading the prior only when needed.
@@ -239,21 +311,20 @@ struct Kron2Fast {
   static constexpr bool BULK = (C::NN * sizeof(T)) % 16 == 0;
   static constexpr int RING = C::IPW * C::SLOT;  // elements per warp stage
   static constexpr size_t smem_bytes() {
-    return sizeof(T) * ((size_t)C::A_ELEMS + (size_t)C::ROW_ELEMS + (size_t)WARPS * STAGES * RING) +
+    return sizeof(T) * ((size_t)C::A_ELEMS + (size_t)WARPS * STAGES * RING) +
            sizeof(unsigned long long) * WARPS * STAGES;
   }
 };
 
 template <typename T, int N, int OPX, int V>
 __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
-    kron2_sq_kernel(const Kron2Params<T> p, const long long ngroups) {
+    kron2_sq_kernel(const Kron2Params<T> p, const __grid_constant__ SqConsts2<T, N> kc, const long long ngroups) {
   using K = Kron2Fast<T, N, V>;
   using C = SqCfg<T, N>;
   constexpr int R = C::R, TPI = C::TPI, IPW = C::IPW, NN = C::NN, VXC = C::VXC, S = K::STAGES;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* ablk = reinterpret_cast<T*>(smem_raw);
-  T* wrow = ablk + C::A_ELEMS;
-  T* ring = wrow + C::ROW_ELEMS;
+  T* ring = ablk + C::A_ELEMS;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(ring + K::WARPS * S * K::RING);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -262,8 +333,7 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
       for (int s = 0; s < S; ++s) mbar_init(&bars[warp * S + s], 1);
     mbar_fence_init();
   }
-  stage_a<T, N>(ablk, p.A, p.lda, p.opa);
-  stage_rows<T, N>(wrow, p.B, p.ldb, p.opb, p.alpha, true);
+  stage_a_param<T, N>(ablk, kc.a);
   __syncthreads();
 
   T* wring = ring + warp * S * K::RING;
@@ -325,7 +395,7 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
 #pragma unroll
         for (int jj = 0; jj < K::JB; ++jj)
           if (j0 + jj < N) init_y<T, N>(y[jj], yb + (long long)(j0 + jj) * p.ldy, rows, p.beta_mode, p.beta);
-        contract_rows<T, N, K::JB>(y, t, wrow, j0);
+        contract_rows_c<T, N, K::JB>(y, t, kc.w, j0);
 #pragma unroll
         for (int jj = 0; jj < K::JB; ++jj)
           if (j0 + jj < N) store_y<T, N>(yb + (long long)(j0 + jj) * p.ldy, y[jj], rows);
@@ -397,6 +467,7 @@ struct Kron3Fast {
   static constexpr int STAGES = V == 3 ? 1 : 2;
   static constexpr int MINB = V == 1 ? 1 : (V == 2 ? 6 : (V == 3 ? 4 : 3));  // resident CTAs/SM targeted
   static constexpr int MB = 4;
+  static constexpr bool AREG = sizeof(T) == 4 && C::R * N <= 64;  // A rows live in registers
   static constexpr int JB = sizeof(T) == 4 ? 4 : 4;
   static constexpr int KB = JB;
   static constexpr bool BULK = (C::NN * sizeof(T)) % 16 == 0;  // one cp.async.bulk per plane
@@ -404,8 +475,7 @@ struct Kron3Fast {
   static constexpr int ITEM = N * PS;                          // entry stride in smem
   static constexpr int TILE = IT * ITEM;
   static constexpr size_t smem_bytes() {
-    return sizeof(T) * ((size_t)C::A_ELEMS + 2 * (size_t)C::ROW_ELEMS + (size_t)STAGES * TILE) +
-           sizeof(unsigned long long) * STAGES;
+    return sizeof(T) * ((size_t)C::A_ELEMS + (size_t)STAGES * TILE) + sizeof(unsigned long long) * STAGES;
   }
 };
 
@@ -440,15 +510,13 @@ __device__ __forceinline__ void sts_rows(T* dst, const T (&v)[SqCfg<T, N>::R], i
 
 template <typename T, int N, int V>
 __global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS, Kron3Fast<T, N, V>::MINB)
-    kron3_sq_kernel(const Kron3Params<T> p, const long long ntiles) {
+    kron3_sq_kernel(const Kron3Params<T> p, const __grid_constant__ SqConsts3<T, N> kc, const long long ntiles) {
   using K = Kron3Fast<T, N, V>;
   using C = SqCfg<T, N>;
   constexpr int R = C::R, TPI = C::TPI, NN = C::NN, VXC = C::VXC, IT = K::IT, PS = K::PS, S = K::STAGES;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* ablk = reinterpret_cast<T*>(smem_raw);
-  T* brow = ablk + C::A_ELEMS;     // B_r rows (stage 1b: alpha 1, exact)
-  T* crow = brow + C::ROW_ELEMS;   // fl(alpha*C_r) rows
-  T* tiles = crow + C::ROW_ELEMS;
+  T* tiles = ablk + C::A_ELEMS;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(tiles + S * K::TILE);
 
   const int tid = threadIdx.x;
@@ -457,9 +525,7 @@ __global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS, Kron3Fast<T, N, V
       for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     mbar_fence_init();
   }
-  stage_a<T, N>(ablk, p.A, p.lda, p.opa);
-  stage_rows<T, N>(brow, p.B, p.ldb, p.opb, T(1), false);
-  stage_rows<T, N>(crow, p.C, p.ldc, p.opc, p.alpha, true);
+  stage_a_param<T, N>(ablk, kc.a);
   __syncthreads();
 
   // start loading tile `tile` (IT entries, N planes each) into `stage`; warp 0 issues
@@ -520,7 +586,13 @@ __global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS, Kron3Fast<T, N, V
     {
       T* xs = buf + te * K::ITEM + tn * PS;
       T t[N][R];
-      mode1<T, N, 0, K::MB>(t, xs, aq);
+      if constexpr (K::AREG) {
+        T ar[N][R];  // reloaded per tile: live only through mode 1
+#pragma unroll
+        for (int l = 0; l < N; ++l) lds_n<R, C::VR>(ar[l], aq + l * R);
+        mode1_areg<T, N, K::MB>(t, xs, ar);
+      } else
+        mode1<T, N, 0, K::MB>(t, xs, aq);
       __syncwarp();  // every lane of this warp finished reading its X plane
 #pragma unroll
       for (int j0 = 0; j0 < N; j0 += K::JB) {
@@ -529,7 +601,7 @@ __global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS, Kron3Fast<T, N, V
         for (int jj = 0; jj < K::JB; ++jj)
 #pragma unroll
           for (int r = 0; r < R; ++r) t2[jj][r] = T(0);
-        contract_rows<T, N, K::JB>(t2, t, brow, j0);
+        contract_rows_c<T, N, K::JB>(t2, t, kc.b, j0);
 #pragma unroll
         for (int jj = 0; jj < K::JB; ++jj)
           if (j0 + jj < N) sts_rows<T, N>(xs + (j0 + jj) * N + q * R, t2[jj], rows);
@@ -563,7 +635,7 @@ __global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS, Kron3Fast<T, N, V
 #pragma unroll
           for (int kk = 0; kk < K::KB; ++kk)
             if (k0 + kk < N) init_y<T, N>(y[kk], yb + (long long)(k0 + kk) * p.ldy2, rows, p.beta_mode, p.beta);
-          contract_rows<T, N, K::KB>(y, f, crow, k0);
+          contract_rows_c<T, N, K::KB>(y, f, kc.c, k0);
 #pragma unroll
           for (int kk = 0; kk < K::KB; ++kk)
             if (k0 + kk < N) store_y<T, N>(yb + (long long)(k0 + kk) * p.ldy2, y[kk], rows);

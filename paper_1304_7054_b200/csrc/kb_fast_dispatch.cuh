@@ -49,7 +49,7 @@ static int env_variant(const char* name) {
 }
 
 template <typename T, int N, int OPX, int V>
-static cudaError_t launch2v(const Kron2Params<T>& p, int sm_count, cudaStream_t s) {
+static cudaError_t launch2v(const Kron2Params<T>& p, const T* ha, const T* hw, int sm_count, cudaStream_t s) {
   using C = SqCfg<T, N>;
   using K = Kron2Fast<T, N, V>;
   if (p.ldx != N || p.sx % C::VXC || !aligned<T>(p.X, C::VXC)) return cudaErrorNotSupported;
@@ -63,26 +63,32 @@ static cudaError_t launch2v(const Kron2Params<T>& p, int sm_count, cudaStream_t 
   const long long ngroups = (p.batch + C::IPW - 1) / C::IPW;
   const long long want = (ngroups + K::WARPS - 1) / K::WARPS;
   const int grid = (int)(want < (long long)sm_count * occ ? want : (long long)sm_count * occ);
-  kern<<<grid, threads, smem, s>>>(p, ngroups);
+  SqConsts2<T, N> kc;
+  for (int i = 0; i < N * N; ++i) {
+    kc.a[i] = ha[i];
+    kc.w[i] = hw[i];
+  }
+  kern<<<grid, threads, smem, s>>>(p, kc, ngroups);
   return cudaGetLastError();
 }
 
 template <typename T, int N, int OPX>
-static cudaError_t launch2(const Kron2Params<T>& p, int sm_count, cudaStream_t s) {
+static cudaError_t launch2(const Kron2Params<T>& p, const T* ha, const T* hw, int sm_count, cudaStream_t s) {
   if constexpr (N == 10 || N == 16) {
     static const int v = env_variant("KB_VARIANT2");
     switch (v) {
-      case 1: return launch2v<T, N, OPX, 1>(p, sm_count, s);
-      case 2: return launch2v<T, N, OPX, 2>(p, sm_count, s);
-      case 3: return launch2v<T, N, OPX, 3>(p, sm_count, s);
+      case 1: return launch2v<T, N, OPX, 1>(p, ha, hw, sm_count, s);
+      case 2: return launch2v<T, N, OPX, 2>(p, ha, hw, sm_count, s);
+      case 3: return launch2v<T, N, OPX, 3>(p, ha, hw, sm_count, s);
       default: break;
     }
   }
-  return launch2v<T, N, OPX, 0>(p, sm_count, s);
+  return launch2v<T, N, OPX, 0>(p, ha, hw, sm_count, s);
 }
 
 template <typename T, int N, int V>
-static cudaError_t launch3v(const Kron3Params<T>& p, int sm_count, cudaStream_t s) {
+static cudaError_t launch3v(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
+                            cudaStream_t s) {
   using C = SqCfg<T, N>;
   using K = Kron3Fast<T, N, V>;
   if (p.ldx != N || p.ldx2 != (long long)N * N || p.sx % C::VXC || !aligned<T>(p.X, C::VXC))
@@ -95,33 +101,40 @@ static cudaError_t launch3v(const Kron3Params<T>& p, int sm_count, cudaStream_t 
   if (occ <= 0) return cudaErrorNotSupported;
   const long long ntiles = (p.batch + K::IT - 1) / K::IT;
   const int grid = (int)(ntiles < (long long)sm_count * occ ? ntiles : (long long)sm_count * occ);
-  kern<<<grid, K::THREADS, smem, s>>>(p, ntiles);
+  SqConsts3<T, N> kc;
+  for (int i = 0; i < N * N; ++i) {
+    kc.a[i] = ha[i];
+    kc.b[i] = hb[i];
+    kc.c[i] = hc[i];
+  }
+  kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
   return cudaGetLastError();
 }
 
 template <typename T, int N>
-static cudaError_t launch3(const Kron3Params<T>& p, int sm_count, cudaStream_t s) {
+static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
+                           cudaStream_t s) {
   if constexpr (N == 10 || N == 16) {
     static const int v = env_variant("KB_VARIANT3");
     switch (v) {
-      case 1: return launch3v<T, N, 1>(p, sm_count, s);
-      case 2: return launch3v<T, N, 2>(p, sm_count, s);
-      case 3: return launch3v<T, N, 3>(p, sm_count, s);
+      case 1: return launch3v<T, N, 1>(p, ha, hb, hc, sm_count, s);
+      case 2: return launch3v<T, N, 2>(p, ha, hb, hc, sm_count, s);
+      case 3: return launch3v<T, N, 3>(p, ha, hb, hc, sm_count, s);
       default: break;
     }
   }
-  return launch3v<T, N, 0>(p, sm_count, s);
+  return launch3v<T, N, 0>(p, ha, hb, hc, sm_count, s);
 }
 
 #define KB_CASE2(N)                                                    \
   case N:                                                              \
-    return p.opx ? launch2<T, N, 1>(p, sm_count, s) : launch2<T, N, 0>(p, sm_count, s);
+    return p.opx ? launch2<T, N, 1>(p, ha, hw, sm_count, s) : launch2<T, N, 0>(p, ha, hw, sm_count, s);
 #define KB_CASE3(N) \
   case N:           \
-    return launch3<T, N>(p, sm_count, s);
+    return launch3<T, N>(p, ha, hb, hc, sm_count, s);
 
 template <typename T>
-cudaError_t launch_kron2_fast(const Kron2Params<T>& p, int sm_count, cudaStream_t s) {
+cudaError_t launch_kron2_fast(const Kron2Params<T>& p, const T* ha, const T* hw, int sm_count, cudaStream_t s) {
   if (p.m_a != p.n_a || p.m_a != p.m_b || p.m_a != p.n_b) return cudaErrorNotSupported;
   switch (p.m_a) {
     KB_CASE2(1) KB_CASE2(2) KB_CASE2(3) KB_CASE2(4) KB_CASE2(5) KB_CASE2(6) KB_CASE2(7) KB_CASE2(8)
@@ -131,7 +144,8 @@ cudaError_t launch_kron2_fast(const Kron2Params<T>& p, int sm_count, cudaStream_
 }
 
 template <typename T>
-cudaError_t launch_kron3_fast(const Kron3Params<T>& p, int sm_count, cudaStream_t s) {
+cudaError_t launch_kron3_fast(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
+                              cudaStream_t s) {
   if (p.m_a != p.n_a || p.m_a != p.m_b || p.m_a != p.n_b || p.m_a != p.m_c || p.m_a != p.n_c)
     return cudaErrorNotSupported;
   switch (p.m_a) {

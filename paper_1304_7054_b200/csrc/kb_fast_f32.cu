@@ -3,6 +3,7 @@
 #include "kb_fast_dispatch.cuh"
 
 namespace kb {
-template cudaError_t launch_kron2_fast<float>(const Kron2Params<float>&, int, cudaStream_t);
-template cudaError_t launch_kron3_fast<float>(const Kron3Params<float>&, int, cudaStream_t);
+template cudaError_t launch_kron2_fast<float>(const Kron2Params<float>&, const float*, const float*, int, cudaStream_t);
+template cudaError_t launch_kron3_fast<float>(const Kron3Params<float>&, const float*, const float*, const float*, int,
+                                              cudaStream_t);
 }  // namespace kb

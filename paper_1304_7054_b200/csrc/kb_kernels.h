@@ -25,10 +25,13 @@ cudaError_t launch_scale(T* Y, long long batch, long long d1, long long d2, long
 // Square n <= 16 register-blocked kernels. Return cudaErrorNotSupported
 // (without launching) when the layout does not meet the fast-path
 // preconditions (tight entries, vector alignment); the caller then uses the
-// generic kernel.
+// generic kernel. The constant matrices come as HOST arrays, op-resolved and
+// alpha-folded (n*n each): ha = A_r col-major, hw/hc = fl(alpha*B_r / C_r)
+// row-major, hb = B_r row-major; they are passed as kernel parameters.
 template <typename T>
-cudaError_t launch_kron2_fast(const Kron2Params<T>& p, int sm_count, cudaStream_t s);
+cudaError_t launch_kron2_fast(const Kron2Params<T>& p, const T* ha, const T* hw, int sm_count, cudaStream_t s);
 template <typename T>
-cudaError_t launch_kron3_fast(const Kron3Params<T>& p, int sm_count, cudaStream_t s);
+cudaError_t launch_kron3_fast(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
+                              cudaStream_t s);
 
 }  // namespace kb

@@ -207,6 +207,40 @@ const T* const_on_device(const T* m, i64 elems, int dev, T* slot, cudaStream_t s
   return slot;
 }
 
+// Host copy of a small constant matrix (device -> host copy when needed; this
+// synchronises the stream, which only the square fast path requires).
+template <typename T>
+std::vector<T> fetch_host(const T* m, i64 elems, cudaStream_t s) {
+  std::vector<T> h((size_t)std::max<i64>(elems, 1));
+  if (elems <= 0) return h;
+  const PtrInfo pi = classify(m);
+  if (pi.device) {
+    cuda_check(cudaMemcpyAsync(h.data(), m, sizeof(T) * (size_t)elems, cudaMemcpyDeviceToHost, s), "constant fetch");
+    cuda_check(cudaStreamSynchronize(s), "constant fetch");
+  } else {
+    std::memcpy(h.data(), m, sizeof(T) * (size_t)elems);
+  }
+  return h;
+}
+
+// Square n x n op-resolution on the host (detail.hpp:19-31) into the kernel
+// parameter layouts: col-major op(M) (`rows` = false) or row-major op(M) scaled
+// by fl(alpha * .) (`rows` = true, the w = alpha*R fold of detail.hpp:53).
+template <typename T>
+std::vector<T> resolve_sq(const std::vector<T>& m, i64 ld, int trans, int n, bool rows, T alpha, bool scale) {
+  std::vector<T> out((size_t)n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const T v = trans ? m[(size_t)(j + i * ld)] : m[(size_t)(i + j * ld)];  // op(M)(i, j)
+      const T w = scale ? static_cast<T>(alpha * v) : v;
+      if (rows)
+        out[(size_t)i * n + j] = w;
+      else
+        out[(size_t)i + (size_t)j * n] = w;
+    }
+  return out;
+}
+
 void count_launch(const char* path) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   t_last_path = path;
@@ -227,8 +261,8 @@ struct K2 {
 
 // Launch the compute for entries [0, n) of device-resident X/Y views.
 template <typename T>
-void run2_device(const K2<T>& k, const T* A, const T* B, const T* X, T* Y, i64 n, DevRes& r, cudaStream_t s,
-                 int slot) {
+void run2_device(const K2<T>& k, const T* A, const T* B, const T* ha, const T* hw, const T* X, T* Y, i64 n,
+                 DevRes& r, cudaStream_t s, int slot) {
   Kron2Params<T> p{};
   p.A = A; p.B = B; p.X = X; p.Y = Y;
   p.lda = k.lda; p.ldb = k.ldb; p.ldx = k.ldx; p.sx = k.sx; p.ldy = k.ldy; p.sy = k.sy;
@@ -237,7 +271,7 @@ void run2_device(const K2<T>& k, const T* A, const T* B, const T* X, T* Y, i64 n
   p.opa = is_t(k.ta); p.opb = is_t(k.tb); p.opx = is_t(k.tx);
   p.beta_mode = beta_mode_of((double)k.beta);
   p.alpha = k.alpha; p.beta = k.beta;
-  cudaError_t e = kb::launch_kron2_fast<T>(p, r.sm_count, s);
+  cudaError_t e = ha ? kb::launch_kron2_fast<T>(p, ha, hw, r.sm_count, s) : cudaErrorNotSupported;
   if (e == cudaSuccess) {
     count_launch("kron2_fast");
     return;
@@ -397,6 +431,7 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
     if (scale_only && beta == T(1)) return KB_OK;
 
     K2<T> k{ta, tb, tx, m_a, n_a, m_b, n_b, batch, alpha, beta, A, lda, B, ldb, X, ldx, ldxp, fpx, Y, ldy, ldyp, fpy};
+    const bool square_fast = m_a == n_a && m_a == m_b && m_a == n_b && m_a >= 1 && m_a <= 16;
     const PtrInfo xi = classify(X), yi = classify(Y);
     const bool x_dev = !scale_only && xi.device, y_dev = yi.device;
     const int dev0 = y_dev ? yi.dev : (x_dev ? xi.dev : current_device());
@@ -407,6 +442,7 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
     auto slice = [&](int dev, i64 p0, i64 p1) {
       const T* Ad = nullptr;
       const T* Bd = nullptr;
+      std::vector<T> ha, hw;  // host-resolved constants for the square fast path
       run_slice(
           dev, X, Y, p0, p1, sp, x_dev && xi.dev == dev, y_dev && yi.dev == dev, us, sync,
           [&](DevRes& r, cudaStream_t s) {
@@ -415,12 +451,17 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
             T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + fb + 64)));
             Ad = const_on_device(A, fa, r.device, cs, s);
             Bd = const_on_device(B, fb, r.device, cs + fa + 32, s);
+            if (square_fast) {
+              ha = resolve_sq(fetch_host(A, fa, s), lda, is_t(ta), (int)m_a, false, T(1), false);
+              hw = resolve_sq(fetch_host(B, fb, s), ldb, is_t(tb), (int)m_a, true, alpha, true);
+            }
           },
           [&](const void* xd, void* yd, i64 n, DevRes& r, cudaStream_t s, int slot) {
             if (scale_only)
               scale2_device<T>(k, static_cast<T*>(yd), n, r, s);
             else
-              run2_device<T>(k, Ad, Bd, static_cast<const T*>(xd), static_cast<T*>(yd), n, r, s, slot);
+              run2_device<T>(k, Ad, Bd, square_fast ? ha.data() : nullptr, square_fast ? hw.data() : nullptr,
+                             static_cast<const T*>(xd), static_cast<T*>(yd), n, r, s, slot);
           });
     };
     if (x_dev || y_dev)
@@ -491,8 +532,11 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
     cudaStream_t us = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
     const bool sync = !(exec && (exec->flags & KB_EXEC_ASYNC) && x_dev && y_dev);
     const i64 fa = fp_matrix(ac, lda), fb = fp_matrix(bc, ldb), fc = fp_matrix(cc, ldc);
+    const bool square_fast = m_a == n_a && m_a == m_b && m_a == n_b && m_a == m_c && m_a == n_c && m_a >= 1 &&
+                             m_a <= 16;
     auto slice = [&](int dev, i64 p0, i64 p1) {
       const T *Ad = nullptr, *Bd = nullptr, *Cd = nullptr;
+      std::vector<T> ha, hb, hc;  // host-resolved constants for the square fast path
       run_slice(dev, X, Y, p0, p1, sp, x_dev && xi.dev == dev, y_dev && yi.dev == dev, us, sync,
                 [&](DevRes& r, cudaStream_t s) {
                   if (scale_only) return;  // A, B, C never read (kron3.hpp:113-128)
@@ -500,6 +544,11 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                   Ad = const_on_device(A, fa, r.device, cs, s);
                   Bd = const_on_device(B, fb, r.device, cs + fa + 32, s);
                   Cd = const_on_device(Cm, fc, r.device, cs + fa + fb + 64, s);
+                  if (square_fast) {
+                    ha = resolve_sq(fetch_host(A, fa, s), lda, is_t(ta), (int)m_a, false, T(1), false);
+                    hb = resolve_sq(fetch_host(B, fb, s), ldb, is_t(tb), (int)m_a, true, T(1), false);
+                    hc = resolve_sq(fetch_host(Cm, fc, s), ldc, is_t(tc), (int)m_a, true, alpha, true);
+                  }
                 },
                 [&](const void* xd, void* yd, i64 n, DevRes& r, cudaStream_t s, int slot) {
                   if (scale_only) {
@@ -519,7 +568,9 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                   p.X = static_cast<const T*>(xd);
                   p.Y = static_cast<T*>(yd);
                   p.batch = n;
-                  cudaError_t e = kb::launch_kron3_fast<T>(p, r.sm_count, s);
+                  cudaError_t e = square_fast
+                                      ? kb::launch_kron3_fast<T>(p, ha.data(), hb.data(), hc.data(), r.sm_count, s)
+                                      : cudaErrorNotSupported;
                   if (e == cudaSuccess) {
                     count_launch("kron3_fast");
                     return;
