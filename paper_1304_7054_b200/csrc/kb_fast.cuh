@@ -303,8 +303,10 @@ template <typename T, int N, int V = 0>
 struct Kron2Fast {
   using C = SqCfg<T, N>;
   static constexpr bool F32 = sizeof(T) == 4;
-  static constexpr int WARPS = V == 0 ? 12 : (V == 1 ? 8 : (V == 2 ? 16 : 12));
-  static constexpr int STAGES = V == 0 ? 2 : (V == 1 ? 3 : (V == 2 ? 1 : 2));
+  // V0 (default): 8 warps x 3 stages (two groups in flight per warp: 6.4 TB/s
+  // at n = 16 fp32); V1: 12 x 2; V2: 16 x 1; V3: 12 x 2 with MB = JB = 2.
+  static constexpr int WARPS = V == 0 ? 8 : (V == 1 ? 12 : (V == 2 ? 16 : 12));
+  static constexpr int STAGES = V == 0 ? 3 : (V == 1 ? 2 : (V == 2 ? 1 : 2));
   static constexpr int MB = V == 3 ? 2 : 4;  // X columns per mode-1 block
   static constexpr int JB = V == 3 ? 2 : 4;  // Y columns per mode-2 block
   // whole entries are 16-byte multiples: one cp.async.bulk per entry
@@ -461,11 +463,14 @@ template <typename T, int N, int V = 0>
 struct Kron3Fast {
   using C = SqCfg<T, N>;
   static constexpr int PT = N * C::TPI;  // threads per entry (one plane task + one fiber block each)
-  static constexpr int MAXT = V == 1 ? 256 : (V == 2 ? 64 : 128);
+  // V0 (default): one entry per 64-thread CTA at n = 16 (barriers span 2 warps,
+  // 6 CTAs/SM); V1: ~128 threads; V2: ~256; V3: ~128, single-stage ring.
+  static constexpr int MAXT = V == 0 ? 64 : (V == 2 ? 256 : 128);
   static constexpr int IT = (MAXT / PT) > 0 ? MAXT / PT : 1;  // entries per tile
   static constexpr int THREADS = IT * PT;
   static constexpr int STAGES = V == 3 ? 1 : 2;
-  static constexpr int MINB = V == 1 ? 1 : (V == 2 ? 6 : (V == 3 ? 4 : 3));  // resident CTAs/SM targeted
+  // resident CTAs/SM targeted (register cap): ~12 warps per SM
+  static constexpr int MINB = V == 3 ? 4 : (384 / THREADS > 0 ? 384 / THREADS : 1);
   static constexpr int MB = 4;
   static constexpr bool AREG = sizeof(T) == 4 && C::R * N <= 64;  // A rows live in registers
   static constexpr int JB = sizeof(T) == 4 ? 4 : 4;
