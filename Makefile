@@ -9,7 +9,8 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -X
 PKG       := paper_1304_7054_b200
 CSRC      := $(PKG)/csrc
 OBJDIR    := build/obj
-SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast_f32.cu $(CSRC)/kb_fast_f64.cu
+SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast_f32.cu $(CSRC)/kb_fast_f64.cu \
+             $(CSRC)/kb_tc.cu
 OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 HDRS      := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/kronbatch_b200.h
 LIB       := $(PKG)/libkronbatch_b200.so

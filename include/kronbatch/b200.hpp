@@ -21,6 +21,7 @@ struct ExecConfig {
   std::vector<std::int32_t> devices;  // >1: shard host-resident batches over these GPUs
   void* stream = nullptr;             // cudaStream_t for device-resident calls
   bool asynchronous = false;          // device buffers only: return before completion
+  bool tf32 = false;                  // allow the 3xTF32 tensor-core kron3 (fp32, n = 16), 1e-5 parity
 };
 
 inline ExecConfig*& current_exec() {
@@ -49,7 +50,7 @@ struct ExecC {
       e.ndevices = static_cast<std::int32_t>(c->devices.size());
       e.devices = c->devices.empty() ? nullptr : c->devices.data();
       e.stream = c->stream;
-      e.flags = c->asynchronous ? KB_EXEC_ASYNC : 0u;
+      e.flags = (c->asynchronous ? KB_EXEC_ASYNC : 0u) | (c->tf32 ? KB_EXEC_TF32 : 0u);
       ptr = &e;
     }
   }

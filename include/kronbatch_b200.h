@@ -61,6 +61,9 @@ enum {
 };
 
 #define KB_EXEC_ASYNC 0x1u /* do not synchronize before returning */
+#define KB_EXEC_TF32 0x2u  /* allow the tcgen05 3xTF32 tensor-core kernel for fp32 kron3 at n = 16
+                              (|err| ~1e-6 relative, within the 1e-5 contract, not bit-exact);
+                              also enabled process-wide by the environment variable KB_TF32=1 */
 
 /* Execution options; pass NULL for the defaults (current device, library
  * stream, synchronous). */

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "libkronbatch_b200.so")
 
 KB_OK, KB_EINVAL, KB_EOVERFLOW, KB_ECUDA, KB_ENOMEM, KB_EINTERNAL = range(6)
 KB_EXEC_ASYNC = 0x1
+KB_EXEC_TF32 = 0x2
 
 ABI_SYMBOLS = (
     "kb_skron2",

@@ -263,6 +263,7 @@ class Exec:
     devices: Sequence[int] = field(default_factory=tuple)
     stream: Any = None
     asynchronous: bool = False
+    tf32: bool = False  # allow the tcgen05 3xTF32 kernel (fp32 kron3, n = 16): 1e-5 parity, not bit-exact
 
     def to_c(self):
         arr = (C.c_int32 * max(1, len(self.devices)))(*self.devices) if self.devices else None
@@ -270,7 +271,8 @@ class Exec:
         if s is not None and hasattr(s, "cuda_stream"):
             s = s.cuda_stream
         ex = _lib.KbExec(len(self.devices), C.cast(arr, C.POINTER(C.c_int32)) if arr is not None else None,
-                         C.c_void_p(s) if s else None, _lib.KB_EXEC_ASYNC if self.asynchronous else 0)
+                         C.c_void_p(s) if s else None,
+                         (_lib.KB_EXEC_ASYNC if self.asynchronous else 0) | (_lib.KB_EXEC_TF32 if self.tf32 else 0))
         return ex, arr
 
 

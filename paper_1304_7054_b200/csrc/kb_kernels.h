@@ -34,4 +34,9 @@ template <typename T>
 cudaError_t launch_kron3_fast(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
                               cudaStream_t s);
 
+// 3-D fp32 n = 16 on tcgen05 tensor cores with 3xTF32 compensation
+// (tolerance-level parity, not bit-exact). Same host constant layouts.
+cudaError_t launch_kron3_tc(const Kron3Params<float>& p, const float* ha, const float* hb, const float* hc,
+                            int sm_count, cudaStream_t s);
+
 }  // namespace kb

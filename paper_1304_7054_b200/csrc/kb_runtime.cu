@@ -14,7 +14,9 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -194,6 +196,14 @@ PtrInfo classify(const void* p) {
     default: break;
   }
   return r;
+}
+
+bool env_tf32() {
+  static const bool on = [] {
+    const char* v = std::getenv("KB_TF32");
+    return v && v[0] == '1';
+  }();
+  return on;
 }
 
 int beta_mode_of(double beta) { return beta == 0.0 ? kb::kBetaZero : (beta == 1.0 ? kb::kBetaOne : kb::kBetaScale); }
@@ -534,6 +544,7 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
     const i64 fa = fp_matrix(ac, lda), fb = fp_matrix(bc, ldb), fc = fp_matrix(cc, ldc);
     const bool square_fast = m_a == n_a && m_a == m_b && m_a == n_b && m_a == m_c && m_a == n_c && m_a >= 1 &&
                              m_a <= 16;
+    const bool use_tf32 = (exec && (exec->flags & KB_EXEC_TF32)) || env_tf32();
     auto slice = [&](int dev, i64 p0, i64 p1) {
       const T *Ad = nullptr, *Bd = nullptr, *Cd = nullptr;
       std::vector<T> ha, hb, hc;  // host-resolved constants for the square fast path
@@ -568,6 +579,17 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                   p.X = static_cast<const T*>(xd);
                   p.Y = static_cast<T*>(yd);
                   p.batch = n;
+                  if constexpr (std::is_same_v<T, float>) {
+                    if (square_fast && m_a == 16 && use_tf32) {
+                      cudaError_t et = kb::launch_kron3_tc(p, ha.data(), hb.data(), hc.data(), r.sm_count, s);
+                      if (et == cudaSuccess) {
+                        count_launch("kron3_tc");
+                        return;
+                      }
+                      if (et != cudaErrorNotSupported) cuda_check(et, "kron3");
+                      cudaGetLastError();
+                    }
+                  }
                   cudaError_t e = square_fast
                                       ? kb::launch_kron3_fast<T>(p, ha.data(), hb.data(), hc.data(), r.sm_count, s)
                                       : cudaErrorNotSupported;
