@@ -6,11 +6,14 @@ NVCC      ?= /usr/local/cuda/bin/nvcc
 CXX_HOST  ?= /usr/bin/g++
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -Xptxas -O3
+ifeq ($(VARIANTS),1)
+NVFLAGS   += -DKB_SWEEP_VARIANTS
+endif
 PKG       := paper_1304_7054_b200
 CSRC      := $(PKG)/csrc
 OBJDIR    := build/obj
-SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast_f32.cu $(CSRC)/kb_fast_f64.cu \
-             $(CSRC)/kb_tc.cu
+SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast2_f32.cu $(CSRC)/kb_fast3_f32.cu \
+             $(CSRC)/kb_fast2_f64.cu $(CSRC)/kb_fast3_f64.cu $(CSRC)/kb_tc.cu
 OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 HDRS      := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/kronbatch_b200.h
 LIB       := $(PKG)/libkronbatch_b200.so

@@ -296,6 +296,58 @@ __device__ __forceinline__ void store_y(T* yc, const T (&y)[SqCfg<T, N>::R], int
   }
 }
 
+// Store R rows (the valid prefix when the block is padded) to smem.
+template <typename T, int N>
+__device__ __forceinline__ void sts_rows(T* dst, const T (&v)[SqCfg<T, N>::R], int rows) {
+  using C = SqCfg<T, N>;
+  constexpr int R = C::R;
+  if (R * C::TPI == N || rows >= R) {
+    if constexpr (C::PLANE_VEC) {
+#pragma unroll
+      for (int r = 0; r < R; r += C::VR) {
+        if constexpr (C::VR * sizeof(T) == 16 && sizeof(T) == 4)
+          *reinterpret_cast<float4*>(dst + r) = make_float4(v[r], v[r + 1], v[r + 2], v[r + 3]);
+        else if constexpr (C::VR * sizeof(T) == 16)
+          *reinterpret_cast<double2*>(dst + r) = make_double2(v[r], v[r + 1]);
+        else if constexpr (C::VR == 2 && sizeof(T) == 4)
+          *reinterpret_cast<float2*>(dst + r) = make_float2(v[r], v[r + 1]);
+        else
+          dst[r] = v[r];
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[r] = v[r];
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (r < rows) dst[r] = v[r];
+  }
+}
+
+// ------------------------------------------------------ staged Y copy-out --
+// Y blocks staged in shared memory (same element layout as the tight global
+// entry / plane) leave with coalesced VW-element vector stores: consecutive
+// threads write consecutive chunks, so a warp instruction covers 32 chunks of
+// one contiguous span instead of 32 scattered R-row pieces. Used when the
+// row-block stores would be narrower than 16 bytes (n % 4 != 0 fp32 ...).
+//   chunk c of `nent` entries x `planes` planes x CPP chunks per plane:
+//   smem  src + e*ent_stride + pl*plane_stride + r*VW
+//   HBM   Y + e*sy + pl*NN + r*VW
+template <typename T, int NN, int VW>
+__device__ __forceinline__ void copy_out(T* __restrict__ Y, long long sy, const T* __restrict__ src, int ent_stride,
+                                         int plane_stride, int planes, int nent, int tid, int nthreads) {
+  constexpr int CPP = NN / VW;
+  const int total = nent * planes * CPP;
+  for (int c = tid; c < total; c += nthreads) {
+    const int ep = c / CPP, r = c - ep * CPP;
+    const int e = ep / planes, pl = ep - e * planes;
+    T v[VW];
+    lds_vec<VW>(v, src + e * ent_stride + pl * plane_stride + r * VW);
+    stg_n<VW, VW>(Y + e * sy + (long long)pl * NN + r * VW, v);
+  }
+}
+
 // ---------------------------------------------------------------- kron2 ---
 
 // Launch/tiling policy; V selects a tuning variant (V = 0 is the default).
@@ -320,7 +372,8 @@ struct Kron2Fast {
 
 template <typename T, int N, int OPX, int V>
 __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
-    kron2_sq_kernel(const Kron2Params<T> p, const __grid_constant__ SqConsts2<T, N> kc, const long long ngroups) {
+    kron2_sq_kernel(const Kron2Params<T> p, const __grid_constant__ SqConsts2<T, N> kc, const long long ngroups,
+                    const int ystage) {
   using K = Kron2Fast<T, N, V>;
   using C = SqCfg<T, N>;
   constexpr int R = C::R, TPI = C::TPI, IPW = C::IPW, NN = C::NN, VXC = C::VXC, S = K::STAGES;
@@ -386,8 +439,33 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
       __syncwarp();
     }
     const long long item = g * IPW + slot;
-    if (item < p.batch) {
-      const T* xs = wring + stage * K::RING + slot * C::SLOT;
+    T* xs = wring + stage * K::RING + slot * C::SLOT;
+    if (ystage) {
+      // Y(I_q, j) goes into the entry's own smem slot (X is dead once every
+      // lane of the entry finished mode 1), then leaves with coalesced stores.
+      T t[N][R];
+      if (item < p.batch) mode1<T, N, OPX, K::MB>(t, xs, aq);
+      __syncwarp();
+      if (item < p.batch) {
+        const T* yb = p.Y + item * p.sy + q * R;
+#pragma unroll
+        for (int j0 = 0; j0 < N; j0 += K::JB) {
+          T y[K::JB][R];
+#pragma unroll
+          for (int jj = 0; jj < K::JB; ++jj)
+            if (j0 + jj < N) init_y<T, N>(y[jj], yb + (long long)(j0 + jj) * p.ldy, rows, p.beta_mode, p.beta);
+          contract_rows_c<T, N, K::JB>(y, t, kc.w, j0);
+#pragma unroll
+          for (int jj = 0; jj < K::JB; ++jj)
+            if (j0 + jj < N) sts_rows<T, N>(xs + (j0 + jj) * N + q * R, y[jj], rows);
+        }
+      }
+      __syncwarp();
+      const long long first = g * IPW;
+      const int valid = (int)(p.batch - first < IPW ? p.batch - first : IPW);
+      copy_out<T, NN, VXC>(p.Y + first * p.sy, p.sy, wring + stage * K::RING, C::SLOT, 0, 1, valid, lane, 32);
+      if constexpr (K::BULK) fence_proxy_async();  // generic smem accesses before the TMA refill
+    } else if (item < p.batch) {
       T t[N][R];
       mode1<T, N, OPX, K::MB>(t, xs, aq);
       T* yb = p.Y + item * p.sy + q * R;
@@ -484,38 +562,10 @@ struct Kron3Fast {
   }
 };
 
-// Store R rows (the valid prefix when the block is padded) to smem.
-template <typename T, int N>
-__device__ __forceinline__ void sts_rows(T* dst, const T (&v)[SqCfg<T, N>::R], int rows) {
-  using C = SqCfg<T, N>;
-  constexpr int R = C::R;
-  if (R * C::TPI == N || rows >= R) {
-    if constexpr (C::PLANE_VEC) {
-#pragma unroll
-      for (int r = 0; r < R; r += C::VR) {
-        if constexpr (C::VR * sizeof(T) == 16 && sizeof(T) == 4)
-          *reinterpret_cast<float4*>(dst + r) = make_float4(v[r], v[r + 1], v[r + 2], v[r + 3]);
-        else if constexpr (C::VR * sizeof(T) == 16)
-          *reinterpret_cast<double2*>(dst + r) = make_double2(v[r], v[r + 1]);
-        else if constexpr (C::VR == 2 && sizeof(T) == 4)
-          *reinterpret_cast<float2*>(dst + r) = make_float2(v[r], v[r + 1]);
-        else
-          dst[r] = v[r];
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < R; ++r) dst[r] = v[r];
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (r < rows) dst[r] = v[r];
-  }
-}
-
 template <typename T, int N, int V>
 __global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS, Kron3Fast<T, N, V>::MINB)
-    kron3_sq_kernel(const Kron3Params<T> p, const __grid_constant__ SqConsts3<T, N> kc, const long long ntiles) {
+    kron3_sq_kernel(const Kron3Params<T> p, const __grid_constant__ SqConsts3<T, N> kc, const long long ntiles,
+                    const int ystage) {
   using K = Kron3Fast<T, N, V>;
   using C = SqCfg<T, N>;
   constexpr int R = C::R, TPI = C::TPI, NN = C::NN, VXC = C::VXC, IT = K::IT, PS = K::PS, S = K::STAGES;
@@ -641,11 +691,26 @@ __global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS, Kron3Fast<T, N, V
           for (int kk = 0; kk < K::KB; ++kk)
             if (k0 + kk < N) init_y<T, N>(y[kk], yb + (long long)(k0 + kk) * p.ldy2, rows, p.beta_mode, p.beta);
           contract_rows_c<T, N, K::KB>(y, f, kc.c, k0);
+          if (ystage) {
+            // Y(I_q, fj, k) overwrites T2(I_q, fj, n = k): exactly the fiber
+            // this thread read above, so no other thread is affected.
+            T* fw = buf + fe * K::ITEM + fj * N + q * R;
 #pragma unroll
-          for (int kk = 0; kk < K::KB; ++kk)
-            if (k0 + kk < N) store_y<T, N>(yb + (long long)(k0 + kk) * p.ldy2, y[kk], rows);
+            for (int kk = 0; kk < K::KB; ++kk)
+              if (k0 + kk < N) sts_rows<T, N>(fw + (k0 + kk) * PS, y[kk], rows);
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < K::KB; ++kk)
+              if (k0 + kk < N) store_y<T, N>(yb + (long long)(k0 + kk) * p.ldy2, y[kk], rows);
+          }
         }
       }
+    }
+    if (ystage) {
+      __syncthreads();
+      const long long first = tile * IT;
+      const int valid = (int)(p.batch - first < IT ? p.batch - first : IT);
+      copy_out<T, NN, VXC>(p.Y + first * p.sy, p.sy, buf, K::ITEM, PS, N, valid, tid, K::THREADS);
     }
     if constexpr (K::BULK) fence_proxy_async();  // generic T2 writes before the next TMA refill
     __syncthreads();

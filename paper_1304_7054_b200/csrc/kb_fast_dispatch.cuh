@@ -42,10 +42,26 @@ static bool aligned(const void* p, int elems) {
   return (reinterpret_cast<uintptr_t>(p) % (sizeof(T) * (size_t)elems)) == 0;
 }
 
-// Development-time variant selection (tools/ sweeps): KB_VARIANT2 / KB_VARIANT3.
-static int env_variant(const char* name) {
+// Development-time variant selection (tools/ sweeps, `make VARIANTS=1`): KB_VARIANT2 / KB_VARIANT3.
+static int env_variant(const char* name, int dflt = 0) {
   const char* v = std::getenv(name);
-  return v ? std::atoi(v) : 0;
+  return v ? std::atoi(v) : dflt;
+}
+
+// Stage Y through shared memory + coalesced copy-out instead of the direct
+// R-row stores. Measured per size on B200 (profiles/r01_sweep_ystage.txt):
+// it pays for 2-D where the row-block stores are narrow and scattered
+// (fp32 n = 5, 6, 7, 9, 10, 14; fp64 n = 3, 5, 6, 7) and loses everywhere
+// else, including every 3-D case (the extra CTA barrier costs more than the
+// store coalescing gains). KB_YSTAGE=0 / 1 forces it off / on for sweeps.
+template <typename T, int N, int DIMS>
+static bool want_ystage(bool legal) {
+  static const int force = env_variant("KB_YSTAGE", -1);
+  if (!legal) return false;
+  if (force >= 0) return force != 0;
+  if (DIMS == 3) return false;
+  if (sizeof(T) == 4) return N == 5 || N == 6 || N == 7 || N == 9 || N == 10 || N == 14;
+  return N == 3 || N == 5 || N == 6 || N == 7;
 }
 
 template <typename T, int N, int OPX, int V>
@@ -68,12 +84,14 @@ static cudaError_t launch2v(const Kron2Params<T>& p, const T* ha, const T* hw, i
     kc.a[i] = ha[i];
     kc.w[i] = hw[i];
   }
-  kern<<<grid, threads, smem, s>>>(p, kc, ngroups);
+  const bool ys = want_ystage<T, N, 2>(p.ldy == N && p.sy % C::VXC == 0 && aligned<T>(p.Y, C::VXC));
+  kern<<<grid, threads, smem, s>>>(p, kc, ngroups, ys ? 1 : 0);
   return cudaGetLastError();
 }
 
 template <typename T, int N, int OPX>
 static cudaError_t launch2(const Kron2Params<T>& p, const T* ha, const T* hw, int sm_count, cudaStream_t s) {
+#ifdef KB_SWEEP_VARIANTS  // tuning variants: built only with `make VARIANTS=1`
   if constexpr (N == 10 || N == 16) {
     static const int v = env_variant("KB_VARIANT2");
     switch (v) {
@@ -83,6 +101,7 @@ static cudaError_t launch2(const Kron2Params<T>& p, const T* ha, const T* hw, in
       default: break;
     }
   }
+#endif
   return launch2v<T, N, OPX, 0>(p, ha, hw, sm_count, s);
 }
 
@@ -107,13 +126,16 @@ static cudaError_t launch3v(const Kron3Params<T>& p, const T* ha, const T* hb, c
     kc.b[i] = hb[i];
     kc.c[i] = hc[i];
   }
-  kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
+  const bool ys = want_ystage<T, N, 3>(p.ldy == N && p.ldy2 == (long long)N * N && p.sy % C::VXC == 0 &&
+                                    aligned<T>(p.Y, C::VXC));
+  kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles, ys ? 1 : 0);
   return cudaGetLastError();
 }
 
 template <typename T, int N>
 static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
                            cudaStream_t s) {
+#ifdef KB_SWEEP_VARIANTS  // tuning variants: built only with `make VARIANTS=1`
   if constexpr (N == 10 || N == 16) {
     static const int v = env_variant("KB_VARIANT3");
     switch (v) {
@@ -123,6 +145,7 @@ static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, co
       default: break;
     }
   }
+#endif
   return launch3v<T, N, 0>(p, ha, hb, hc, sm_count, s);
 }
 
