@@ -1,0 +1,299 @@
+// kb_cw3.cuh -- "column-wise" square 3-D kernel (kron3, even n <= 16).
+//
+// Same arithmetic as the reference stage order (kron3.hpp:147-163, each
+// gemm_axpy_fixed of detail.hpp:38-59 an ascending FMA chain per element),
+// re-mapped so that EVERY contraction takes its shared operand from the
+// constant bank (uniform registers) instead of registers or shared memory:
+//
+//   mode 1 (column owner):  T1(:, m, n) = A_r * X(:, m, n)
+//     a thread owns whole X columns (CA of them); FFMA2 pairs two ROWS i, i+1
+//     of its column: {T1(i,m,n), T1(i+1,m,n)} += {A(i,l), A(i+1,l)} * X(l,m,n)
+//     -- the A pair is a uniform-register pair (SASS `FFMA2 R, R.F32,
+//     UR.F32x2`), the X element a per-thread scalar. T1 overwrites the X
+//     column in shared memory (same thread, same addresses).
+//   mode 2 (row owner, R = 2): T2(I_q, j, n) = sum_m T1(I_q, m, n) B_r(j, m)
+//     row pair from smem x uniform scalar B_r(j, m); overwrites T1(I_q, :, n).
+//   mode 3 (row owner, R = 2): Y(I_q, j, k) = init + sum_n T2(I_q, j, n) Cw(k, n)
+//     with Cw = fl(alpha * C_r); Y leaves registers straight to HBM.
+//
+// Versus kb_fast.cuh's kron3_sq_kernel this drops the A rows held in
+// registers (64 per thread) and most broadcast LDS traffic, so a tile runs
+// with ~80 registers per thread and twice the warps per SM. Tiles of IT
+// entries land by one cp.async.bulk per plane into a padded plane stride PS
+// chosen so that all three phases' shared-memory accesses are conflict-free.
+#pragma once
+
+#include "kb_fast.cuh"
+
+namespace kb {
+
+template <typename T, int N>
+struct SqConstsCw3 {
+  T a[N * N];   // a[l*N + i]  = A_r(i, l)          (column l contiguous: row pairs)
+  T bt[N * N];  // bt[m*N + j] = B_r(j, m)          (all j of one m contiguous)
+  T ct[N * N];  // ct[n*N + k] = fl(alpha*C_r(k, n))
+};
+
+// Bank multiplicity of one shared-memory access phase: `lanes` lanes, lane k at
+// word offset off(k) (4-byte words), each touching `words` consecutive words.
+// Identical addresses broadcast.
+template <typename F>
+__host__ __device__ constexpr int phase_banks(F off, int lanes, int words) {
+  int cnt[32] = {};
+  int worst = 0;
+  for (int k = 0; k < lanes; ++k) {
+    bool dup = false;
+    for (int k2 = 0; k2 < k && !dup; ++k2) dup = off(k2) == off(k);
+    if (dup) continue;
+    for (int w = 0; w < words; ++w) {
+      const int b = (int)((off(k) + w) % 32);
+      if (++cnt[b] > worst) worst = cnt[b];
+    }
+  }
+  return worst;
+}
+
+template <typename T, int N, int V = 0>
+struct Cw3 {
+  static_assert(N % 2 == 0, "column-wise kernel: even n");
+  static constexpr int ES = sizeof(T);
+  static constexpr int R = 2;                 // rows per mode-2/3 task
+  static constexpr int TPI = N / R;           // tasks per plane / per fiber column
+  static constexpr int NN = N * N;
+  // entries per tile: ~256 threads of mode-2/3 tasks (fp32), 128 (fp64)
+  static constexpr int MAXT = ES == 4 ? 256 : 128;
+  static constexpr int IT = MAXT / (N * TPI) > 0 ? MAXT / (N * TPI) : 1;
+  static constexpr int NP = IT * N;           // planes per tile
+  static constexpr int NTASK = NP * TPI;      // mode-2 and mode-3 tasks per tile
+  static constexpr int THREADS = (NTASK + 31) / 32 * 32;
+  static constexpr int NCOL = NP * N;         // mode-1 columns per tile
+  static constexpr int CA = (NCOL + THREADS - 1) / THREADS;
+  static constexpr int STAGES = V == 1 ? 1 : 2;
+  static constexpr int MINB = ES == 4 ? (V == 1 ? 4 : 3) : (V == 1 ? 6 : 3);
+  static constexpr int VXR = vec_width(N, ES);  // column read width (elements)
+  static constexpr int VR = vec_width(R, ES);   // row-pair width
+  static constexpr bool BULK = (NN * ES) % 16 == 0;
+  // mode-2 plane permutation: 4 plane groups of a warp's 16-lane phases
+  // spread across the banks (see plane_of_task)
+  static constexpr bool PERM = N % 4 == 0 && TPI * 4 <= 32;
+
+  __host__ __device__ static constexpr int plane_of_group(int g) {
+    if (!PERM) return g;
+    const int e = g / N, gi = g % N;
+    return e * N + gi / 4 + (N / 4) * (gi % 4);
+  }
+
+  // worst bank multiplicity over the three phases for plane stride ps (elements)
+  __host__ __device__ static constexpr int conflicts(int ps) {
+    const int wpe = ES / 4;  // words per element
+    const int item = N * ps;
+    int worst = 1;
+    // mode-1 column reads: lanes 0..(128/(VXR*ES))-1 own columns c = lane
+    {
+      const int lanes = 128 / (VXR * ES) < 32 ? 128 / (VXR * ES) : 32;
+      auto off = [&](int k) {
+        const int P = k % NP, m = k / NP;
+        return ((P / N) * item + (P % N) * ps + m * N) * wpe;
+      };
+      const int c = phase_banks(off, lanes, VXR * wpe);
+      worst = c > worst ? c : worst;
+    }
+    // mode-2 row-pair reads: task t -> (group g = t / TPI, q = t % TPI), m = 0
+    {
+      const int lanes = 128 / (VR * ES) < 32 ? 128 / (VR * ES) : 32;
+      auto off = [&](int k) {
+        const int P = plane_of_group(k / TPI), q = k % TPI;
+        return ((P / N) * item + (P % N) * ps + q * R) * wpe;
+      };
+      const int c = phase_banks(off, lanes, VR * wpe);
+      worst = c > worst ? c : worst;
+    }
+    return worst;
+  }
+  __host__ __device__ static constexpr int plane_stride() {
+    const int align = BULK ? 16 / ES : VXR;
+    int best = (NN + align - 1) / align * align, best_c = 1 << 30;
+    for (int s = best; s <= best + 64 * align; s += align) {
+      const int c = conflicts(s);
+      if (c < best_c) {
+        best_c = c;
+        best = s;
+        if (c == 1) break;
+      }
+    }
+    return best;
+  }
+  static constexpr int PS = plane_stride();
+  static constexpr int ITEM = N * PS;
+  static constexpr int TILE = IT * ITEM;
+  static constexpr size_t smem_bytes() { return (size_t)ES * STAGES * TILE + 8 * STAGES; }
+};
+
+// {acc[i], acc[i+1]} += {a[i], a[i+1]} * s  (a from the constant bank: FFMA2 with a UR pair)
+__device__ __forceinline__ void axpy_pairs_c(float* acc, const float* a, float s, int n) {
+#pragma unroll
+  for (int i = 0; i < n; i += 2) {
+    const float2 d = ffma2_s(make_float2(a[i], a[i + 1]), s, make_float2(acc[i], acc[i + 1]));
+    acc[i] = d.x;
+    acc[i + 1] = d.y;
+  }
+}
+__device__ __forceinline__ void axpy_pairs_c(double* acc, const double* a, double s, int n) {
+#pragma unroll
+  for (int i = 0; i < n; ++i) acc[i] = __fma_rn(a[i], s, acc[i]);
+}
+
+template <typename T, int N, int V>
+__global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
+    kron3_cw_kernel(const Kron3Params<T> p, const __grid_constant__ SqConstsCw3<T, N> kc, const long long ntiles) {
+  using K = Cw3<T, N, V>;
+  constexpr int R = K::R, TPI = K::TPI, NN = K::NN, IT = K::IT, NP = K::NP, PS = K::PS, S = K::STAGES;
+  constexpr int ITEM = K::ITEM;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tiles = reinterpret_cast<T*>(smem_raw);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(tiles + S * K::TILE);
+  const int tid = threadIdx.x;
+  if (tid == 0)
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+  mbar_fence_init();
+  __syncthreads();
+
+  auto issue = [&](long long tile, int stage) {
+    if (tile >= ntiles || tid >= 32) return;
+    T* dst = tiles + stage * K::TILE;
+    const long long first = tile * IT;
+    const int valid = (int)(p.batch - first < IT ? p.batch - first : IT);
+    if (tid == 0) mbar_arrive_expect_tx(&bars[stage], (unsigned)(valid * N * NN * sizeof(T)));
+    __syncwarp();
+    for (int pl = tid; pl < valid * N; pl += 32) {
+      const int e = pl / N, n = pl - e * N;
+      bulk_g2s(dst + e * ITEM + n * PS, p.X + (first + e) * p.sx + (long long)n * NN, NN * sizeof(T), &bars[stage]);
+    }
+  };
+
+  // per-thread task coordinates (fixed for the kernel)
+  const bool task_ok = tid < K::NTASK;
+  const int q = tid % TPI;
+  const int P2 = K::plane_of_group(tid / TPI);                  // mode-2 plane (entry-major)
+  const int j3 = (tid / TPI) % N, e3 = tid / (TPI * N);        // mode-3 fiber column / entry
+
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) issue(blockIdx.x + (long long)s * gridDim.x, s);
+  int stage = 0;
+  unsigned phase = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if constexpr (S == 1)
+      issue(tile, 0);
+    else
+      issue(tile + (long long)(S - 1) * gridDim.x, (stage + S - 1) % S);
+    mbar_wait(&bars[stage], phase);
+    T* buf = tiles + stage * K::TILE;
+    const long long first = tile * IT;
+    const int valid = (int)(p.batch - first < IT ? p.batch - first : IT);
+
+    // ---- mode 1: columns c = tid + k*THREADS (plane P = c % NP, column m = c / NP)
+    {
+      T acc[K::CA][N];
+      T* col[K::CA];
+#pragma unroll
+      for (int k = 0; k < K::CA; ++k) {
+        const int c = tid + k * K::THREADS;
+        const int P = c % NP, m = c / NP;
+        col[k] = buf + (P / N) * ITEM + (P % N) * PS + m * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) acc[k][i] = T(0);
+      }
+#pragma unroll
+      for (int l0 = 0; l0 < N; l0 += K::VXR) {
+        T x[K::CA][K::VXR];
+#pragma unroll
+        for (int k = 0; k < K::CA; ++k)
+          if (K::CA * K::THREADS == K::NCOL || tid + k * K::THREADS < K::NCOL) lds_vec<K::VXR>(x[k], col[k] + l0);
+#pragma unroll
+        for (int ll = 0; ll < K::VXR; ++ll)
+#pragma unroll
+          for (int k = 0; k < K::CA; ++k) axpy_pairs_c(acc[k], kc.a + (l0 + ll) * N, x[k][ll], N);
+      }
+#pragma unroll
+      for (int k = 0; k < K::CA; ++k)
+        if (K::CA * K::THREADS == K::NCOL || tid + k * K::THREADS < K::NCOL)
+#pragma unroll
+          for (int i = 0; i < N; i += K::VXR) {
+            T v[K::VXR];
+#pragma unroll
+            for (int u = 0; u < K::VXR; ++u) v[u] = acc[k][i + u];
+            if constexpr (K::VXR * sizeof(T) == 16 && sizeof(T) == 4)
+              *reinterpret_cast<float4*>(col[k] + i) = make_float4(v[0], v[1], v[2], v[3]);
+            else if constexpr (K::VXR * sizeof(T) == 16)
+              *reinterpret_cast<double2*>(col[k] + i) = make_double2(v[0], v[1]);
+            else if constexpr (K::VXR == 2 && sizeof(T) == 4)
+              *reinterpret_cast<float2*>(col[k] + i) = make_float2(v[0], v[1]);
+            else
+#pragma unroll
+              for (int u = 0; u < K::VXR; ++u) col[k][i + u] = v[u];
+          }
+    }
+    __syncthreads();
+
+    // ---- mode 2: T2(I_q, j, P2) = sum_m T1(I_q, m, P2) B_r(j, m), in place
+    if (task_ok) {
+      T* pl = buf + (P2 / N) * ITEM + (P2 % N) * PS + q * R;
+      T acc[N][R];
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[j][r] = T(0);
+#pragma unroll
+      for (int m = 0; m < N; ++m) {
+        T t[R];
+        lds_vec<K::VR>(t, pl + m * N);
+#pragma unroll
+        for (int j = 0; j < N; ++j) axpy_rows<R>(acc[j], t, kc.bt[m * N + j]);
+      }
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        if constexpr (sizeof(T) == 4)
+          *reinterpret_cast<float2*>(pl + j * N) = make_float2(acc[j][0], acc[j][1]);
+        else
+          *reinterpret_cast<double2*>(pl + j * N) = make_double2(acc[j][0], acc[j][1]);
+      }
+    }
+    __syncthreads();
+
+    // ---- mode 3: Y(I_q, j3, k) = init + sum_n T2(I_q, j3, n) Cw(k, n)
+    if (task_ok && e3 < valid) {
+      const T* fb = buf + e3 * ITEM + j3 * N + q * R;
+      T* yb = p.Y + (first + e3) * p.sy + (long long)j3 * p.ldy + q * R;
+      T acc[N][R];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        if (p.beta_mode == kBetaZero) {
+          acc[k][0] = T(0);
+          acc[k][1] = T(0);
+        } else {
+          T y0[R];
+          ldg_n<R, K::VR>(y0, yb + (long long)k * p.ldy2);
+          acc[k][0] = beta_init(p.beta_mode, p.beta, y0[0]);
+          acc[k][1] = beta_init(p.beta_mode, p.beta, y0[1]);
+        }
+      }
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        T f[R];
+        lds_vec<K::VR>(f, fb + n * PS);
+#pragma unroll
+        for (int k = 0; k < N; ++k) axpy_rows<R>(acc[k], f, kc.ct[n * N + k]);
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) stg_n<R, K::VR>(yb + (long long)k * p.ldy2, acc[k]);
+    }
+    fence_proxy_async();  // generic smem writes before the stage's next TMA refill
+    __syncthreads();
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+}
+
+}  // namespace kb

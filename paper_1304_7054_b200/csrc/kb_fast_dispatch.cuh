@@ -8,6 +8,7 @@
 #include <map>
 #include <utility>
 
+#include "kb_cw3.cuh"
 #include "kb_fast.cuh"
 #include "kb_kernels.h"
 
@@ -132,9 +133,54 @@ static cudaError_t launch3v(const Kron3Params<T>& p, const T* ha, const T* hb, c
   return cudaGetLastError();
 }
 
+// Column-wise 3-D kernel (kb_cw3.cuh), even n.
+template <typename T, int N, int V>
+static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
+                             cudaStream_t s) {
+  using K = Cw3<T, N, V>;
+  if (p.ldx != N || p.ldx2 != (long long)N * N || (p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))
+    return cudaErrorNotSupported;
+  if (p.ldy % 2 || p.ldy2 % 2 || p.sy % 2 || !aligned<T>(p.Y, 2)) return cudaErrorNotSupported;
+  auto kern = kron3_cw_kernel<T, N, V>;
+  const size_t smem = K::smem_bytes();
+  const int occ = occupancy_for(kern, K::THREADS, smem);
+  if (occ <= 0) return cudaErrorNotSupported;
+  const long long ntiles = (p.batch + K::IT - 1) / K::IT;
+  const int grid = (int)(ntiles < (long long)sm_count * occ ? ntiles : (long long)sm_count * occ);
+  SqConstsCw3<T, N> kc;
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j) {
+      kc.a[i + j * N] = ha[i + j * N];
+      kc.bt[j * N + i] = hb[i * N + j];  // bt[m*N + j] = B_r(j, m)
+      kc.ct[j * N + i] = hc[i * N + j];  // ct[n*N + k] = Cw(k, n)
+    }
+  kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
+  return cudaGetLastError();
+}
+
+// 3-D kernel family per size: 0 = row-owner (kron3_sq_kernel), 1 = column-wise,
+// 2 = column-wise single stage. KB_K3 overrides the default for sweeps.
+template <typename T, int N>
+static int k3_family() {
+  static const int force = env_variant("KB_K3", -1);
+  if (N % 2 || N < 8) return 0;
+  if (force >= 0) return force;
+  // measured on B200 (profiles/r01_k3_families.txt)
+  if (sizeof(T) == 4) return (N == 10 || N == 12 || N == 14) ? 1 : 0;
+  return N == 16 ? 2 : 1;
+}
+
 template <typename T, int N>
 static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
                            cudaStream_t s) {
+  if constexpr (N % 2 == 0 && N >= 8) {
+    const int fam = k3_family<T, N>();
+    if (fam == 1 || fam == 2) {
+      const cudaError_t e = fam == 1 ? launch3cw<T, N, 0>(p, ha, hb, hc, sm_count, s)
+                                     : launch3cw<T, N, 1>(p, ha, hb, hc, sm_count, s);
+      if (e != cudaErrorNotSupported) return e;
+    }
+  }
 #ifdef KB_SWEEP_VARIANTS  // tuning variants: built only with `make VARIANTS=1`
   if constexpr (N == 10 || N == 16) {
     static const int v = env_variant("KB_VARIANT3");

@@ -1,0 +1,19 @@
+"""Kernel-selection switches that are not the default for every size must stay
+bit-exact too: Y staged through shared memory (KB_YSTAGE=1) and direct R-row
+stores (KB_YSTAGE=0); the 3-D kernel families (KB_K3=0 row-owner, 1/2
+column-wise double/single stage) -- every square n, 2-D/3-D, fp32/fp64 (-m gpu)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("env", [{"KB_YSTAGE": "1"}, {"KB_YSTAGE": "0"}, {"KB_K3": "0"}, {"KB_K3": "1"}, {"KB_K3": "2"}])
+def test_kernel_switches_bitwise(env):
+    r = subprocess.run([sys.executable, os.path.join(HERE, "variant_check.py")], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
