@@ -158,8 +158,63 @@ static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, 
   return cudaGetLastError();
 }
 
+// n = 16 warp-plane column-wise kernel (kb_cw3.cuh), S stages.
+template <typename T, int S, bool EARLY>
+static cudaError_t launch3cwp(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
+                              cudaStream_t s) {
+  constexpr int N = 16;
+  using K = Cwp3<T, S, EARLY>;
+  if (p.ldx != N || p.ldx2 != (long long)N * N || (p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))
+    return cudaErrorNotSupported;
+  if (p.ldy % 2 || p.ldy2 % 2 || p.sy % 2 || !aligned<T>(p.Y, 2)) return cudaErrorNotSupported;
+  auto kern = kron3_cwp_kernel<T, S, EARLY>;
+  const size_t smem = K::smem_bytes();
+  const int occ = occupancy_for(kern, K::THREADS, smem);
+  if (occ <= 0) return cudaErrorNotSupported;
+  const long long ntiles = p.batch;
+  const int grid = (int)(ntiles < (long long)sm_count * occ ? ntiles : (long long)sm_count * occ);
+  SqConstsCw3<T, N> kc;
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j) {
+      kc.a[i + j * N] = ha[i + j * N];
+      kc.bt[j * N + i] = hb[i * N + j];
+      kc.ct[j * N + i] = hc[i * N + j];
+    }
+  kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t launch3cwpp(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
+                               cudaStream_t s) {
+  constexpr int N = 16;
+  using K = Cwpp3<T>;
+  if (p.ldx != N || p.ldx2 != (long long)N * N || (p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))
+    return cudaErrorNotSupported;
+  if (p.ldy % 2 || p.ldy2 % 2 || p.sy % 2 || !aligned<T>(p.Y, 2)) return cudaErrorNotSupported;
+  auto kern = kron3_cwpp_kernel<T>;
+  const size_t smem = K::smem_bytes();
+  const int occ = occupancy_for(kern, K::THREADS, smem);
+  if (occ <= 0) return cudaErrorNotSupported;
+  const long long ntiles = p.batch;
+  const int grid = (int)(ntiles < (long long)sm_count * occ ? ntiles : (long long)sm_count * occ);
+  SqConstsCw3<T, N> kc;
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j) {
+      kc.a[i + j * N] = ha[i + j * N];
+      kc.bt[j * N + i] = hb[i * N + j];
+      kc.ct[j * N + i] = hc[i * N + j];
+    }
+  kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
+  return cudaGetLastError();
+}
+
 // 3-D kernel family per size: 0 = row-owner (kron3_sq_kernel), 1 = column-wise,
-// 2 = column-wise single stage. KB_K3 overrides the default for sweeps.
+// 2 = column-wise single stage, 3 = column-wise 128-thread tiles (fp32; = 1 for
+// fp64), 4 / 5 = n = 16 warp-plane kernel with 2 / 1 stages, 6 = n = 16
+// software-pipelined warp-plane kernel (3 stages), 7 / 8 = warp-plane with the
+// early stage release (1 / 2 stages). KB_K3 overrides
+// the default for sweeps.
 template <typename T, int N>
 static int k3_family() {
   static const int force = env_variant("KB_K3", -1);
@@ -175,9 +230,23 @@ static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, co
                            cudaStream_t s) {
   if constexpr (N % 2 == 0 && N >= 8) {
     const int fam = k3_family<T, N>();
-    if (fam == 1 || fam == 2) {
-      const cudaError_t e = fam == 1 ? launch3cw<T, N, 0>(p, ha, hb, hc, sm_count, s)
-                                     : launch3cw<T, N, 1>(p, ha, hb, hc, sm_count, s);
+    if constexpr (N == 16) {
+      if (fam == 6) {
+        const cudaError_t e = launch3cwpp<T>(p, ha, hb, hc, sm_count, s);
+        if (e != cudaErrorNotSupported) return e;
+      }
+      if (fam == 4 || fam == 5 || fam == 7 || fam == 8) {
+        const cudaError_t e = fam == 4   ? launch3cwp<T, 2, false>(p, ha, hb, hc, sm_count, s)
+                              : fam == 5 ? launch3cwp<T, 1, false>(p, ha, hb, hc, sm_count, s)
+                              : fam == 7 ? launch3cwp<T, 1, true>(p, ha, hb, hc, sm_count, s)
+                                         : launch3cwp<T, 2, true>(p, ha, hb, hc, sm_count, s);
+        if (e != cudaErrorNotSupported) return e;
+      }
+    }
+    if (fam >= 1 && fam <= 3) {
+      const cudaError_t e = fam == 1   ? launch3cw<T, N, 0>(p, ha, hb, hc, sm_count, s)
+                            : fam == 2 ? launch3cw<T, N, 1>(p, ha, hb, hc, sm_count, s)
+                                       : launch3cw<T, N, 2>(p, ha, hb, hc, sm_count, s);
       if (e != cudaErrorNotSupported) return e;
     }
   }

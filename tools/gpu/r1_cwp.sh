@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_variants.py -m gpu -q -x 2>&1 | tail -3
+for f in 0 1 2 3 4 5; do
+  for cfg in "16 f32 262144" "16 f64 131072"; do
+    set -- $cfg; KB_K3=$f timeout 120 python tools/quickbench.py one 3 $1 $2 $3 10 2>&1 | sed "s/^/K3=$f /"
+  done
+done
+KB_K3=4 timeout 300 ncu --set full --clock-control none --import-source on -k regex:kron3_cw -s 3 -c 1 -o gpurun_out/cwp4_f32_n16 python tools/quickbench.py one 3 16 f32 262144 1 > /dev/null 2>&1
+KB_K3=5 timeout 300 ncu --set full --clock-control none --import-source on -k regex:kron3_cw -s 3 -c 1 -o gpurun_out/cwp5_f64_n16 python tools/quickbench.py one 3 16 f64 131072 1 > /dev/null 2>&1
