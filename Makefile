@@ -12,8 +12,8 @@ endif
 PKG       := paper_1304_7054_b200
 CSRC      := $(PKG)/csrc
 OBJDIR    := build/obj
-SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast2_f32.cu $(CSRC)/kb_fast3_f32.cu \
-             $(CSRC)/kb_fast2_f64.cu $(CSRC)/kb_fast3_f64.cu $(CSRC)/kb_tc.cu
+SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast_switch.cu $(CSRC)/kb_tc.cu \
+             $(sort $(wildcard $(CSRC)/kb_sz*.cu))
 OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 HDRS      := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/kronbatch_b200.h
 LIB       := $(PKG)/libkronbatch_b200.so

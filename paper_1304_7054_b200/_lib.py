@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkronbatch_b200.so")
+# KB_LIB_PATH: load an alternative in-tree build (A/B kernel experiments under tools/)
+LIB_PATH = os.environ.get("KB_LIB_PATH") or os.path.join(HERE, "libkronbatch_b200.so")
 
 KB_OK, KB_EINVAL, KB_EOVERFLOW, KB_ECUDA, KB_ENOMEM, KB_EINTERNAL = range(6)
 KB_EXEC_ASYNC = 0x1

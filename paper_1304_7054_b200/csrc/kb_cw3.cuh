@@ -25,7 +25,13 @@
 
 #include "kb_fast.cuh"
 
+#ifndef KB_CW_UNROLL
+#define KB_CW_UNROLL 16  // contraction-loop unroll of the column-wise kernels (code size vs loop overhead)
+#endif
+
 namespace kb {
+
+constexpr int kCwUnroll = KB_CW_UNROLL;
 
 template <typename T, int N>
 struct SqConstsCw3 {
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
 #pragma unroll
         for (int i = 0; i < N; ++i) acc[k][i] = T(0);
       }
-#pragma unroll
+#pragma unroll kCwUnroll
       for (int l0 = 0; l0 < N; l0 += K::VXR) {
         T x[K::CA][K::VXR];
 #pragma unroll
@@ -245,7 +251,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
       for (int j = 0; j < N; ++j)
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[j][r] = T(0);
-#pragma unroll
+#pragma unroll kCwUnroll
       for (int m = 0; m < N; ++m) {
         T t[R];
         lds_vec<K::VR>(t, pl + m * N);
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
           acc[k][1] = beta_init(p.beta_mode, p.beta, y0[1]);
         }
       }
-#pragma unroll
+#pragma unroll kCwUnroll
       for (int n = 0; n < N; ++n) {
         T f[R];
         lds_vec<K::VR>(f, fb + n * PS);

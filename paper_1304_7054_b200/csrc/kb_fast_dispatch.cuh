@@ -11,6 +11,7 @@
 #include "kb_cw3.cuh"
 #include "kb_fast.cuh"
 #include "kb_kernels.h"
+#include "kb_sizes.h"
 
 namespace kb {
 
@@ -218,18 +219,19 @@ static cudaError_t launch3cwpp(const Kron3Params<T>& p, const T* ha, const T* hb
 template <typename T, int N>
 static int k3_family() {
   static const int force = env_variant("KB_K3", -1);
-  if (N % 2 || N < 8) return 0;
+  if (N % 2 || N < 4) return 0;
   if (force >= 0) return force;
   // measured on B200 (profiles/r01_k3_families.txt)
-  if (sizeof(T) == 4) return (N == 10 || N == 12 || N == 14) ? 1 : 0;
-  return N == 16 ? 2 : 1;
+  if (sizeof(T) == 4) return N == 16 ? 3 : ((N == 10 || N == 12 || N == 14) ? 1 : 0);
+  return N == 16 ? 2 : (N >= 10 ? 1 : 0);
 }
 
 template <typename T, int N>
 static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
                            cudaStream_t s) {
-  if constexpr (N % 2 == 0 && N >= 8) {
+  if constexpr (N % 2 == 0 && N >= 4) {
     const int fam = k3_family<T, N>();
+#ifdef KB_SWEEP_VARIANTS  // n = 16 warp-plane experiments (profiles/r01_k3_families.txt): `make VARIANTS=1`
     if constexpr (N == 16) {
       if (fam == 6) {
         const cudaError_t e = launch3cwpp<T>(p, ha, hb, hc, sm_count, s);
@@ -243,6 +245,7 @@ static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, co
         if (e != cudaErrorNotSupported) return e;
       }
     }
+#endif
     if (fam >= 1 && fam <= 3) {
       const cudaError_t e = fam == 1   ? launch3cw<T, N, 0>(p, ha, hb, hc, sm_count, s)
                             : fam == 2 ? launch3cw<T, N, 1>(p, ha, hb, hc, sm_count, s)
@@ -264,36 +267,16 @@ static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, co
   return launch3v<T, N, 0>(p, ha, hb, hc, sm_count, s);
 }
 
-#define KB_CASE2(N)                                                    \
-  case N:                                                              \
-    return p.opx ? launch2<T, N, 1>(p, ha, hw, sm_count, s) : launch2<T, N, 0>(p, ha, hw, sm_count, s);
-#define KB_CASE3(N) \
-  case N:           \
-    return launch3<T, N>(p, ha, hb, hc, sm_count, s);
-
-template <typename T>
-cudaError_t launch_kron2_fast(const Kron2Params<T>& p, const T* ha, const T* hw, int sm_count, cudaStream_t s) {
-  if (p.m_a != p.n_a || p.m_a != p.m_b || p.m_a != p.n_b) return cudaErrorNotSupported;
-  switch (p.m_a) {
-    KB_CASE2(1) KB_CASE2(2) KB_CASE2(3) KB_CASE2(4) KB_CASE2(5) KB_CASE2(6) KB_CASE2(7) KB_CASE2(8)
-    KB_CASE2(9) KB_CASE2(10) KB_CASE2(11) KB_CASE2(12) KB_CASE2(13) KB_CASE2(14) KB_CASE2(15) KB_CASE2(16)
-    default: return cudaErrorNotSupported;
-  }
+// Per-size entry points (explicitly instantiated in the kb_sz*.cu compile
+// units, one group of sizes each, so nvcc builds them in parallel); the
+// size switch lives in kb_fast_switch.cu.
+template <typename T, int N>
+cudaError_t kron2_size(const Kron2Params<T>& p, const T* ha, const T* hw, int sm_count, cudaStream_t s) {
+  return p.opx ? launch2<T, N, 1>(p, ha, hw, sm_count, s) : launch2<T, N, 0>(p, ha, hw, sm_count, s);
 }
-
-template <typename T>
-cudaError_t launch_kron3_fast(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
-                              cudaStream_t s) {
-  if (p.m_a != p.n_a || p.m_a != p.m_b || p.m_a != p.n_b || p.m_a != p.m_c || p.m_a != p.n_c)
-    return cudaErrorNotSupported;
-  switch (p.m_a) {
-    KB_CASE3(1) KB_CASE3(2) KB_CASE3(3) KB_CASE3(4) KB_CASE3(5) KB_CASE3(6) KB_CASE3(7) KB_CASE3(8)
-    KB_CASE3(9) KB_CASE3(10) KB_CASE3(11) KB_CASE3(12) KB_CASE3(13) KB_CASE3(14) KB_CASE3(15) KB_CASE3(16)
-    default: return cudaErrorNotSupported;
-  }
+template <typename T, int N>
+cudaError_t kron3_size(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count, cudaStream_t s) {
+  return launch3<T, N>(p, ha, hb, hc, sm_count, s);
 }
-
-#undef KB_CASE2
-#undef KB_CASE3
 
 }  // namespace kb

@@ -1,0 +1,9 @@
+// kb_sz3_f32_n8_9.cu -- float kron3 kernels for n = 8, 9 (one compile unit per size group).
+#include "kb_fast_dispatch.cuh"
+
+namespace kb {
+template cudaError_t kron3_size<float, 8>(const Kron3Params<float>&, const float*, const float*, const float*, int,
+                                          cudaStream_t);
+template cudaError_t kron3_size<float, 9>(const Kron3Params<float>&, const float*, const float*, const float*, int,
+                                          cudaStream_t);
+}  // namespace kb
