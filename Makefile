@@ -18,7 +18,7 @@ OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 HDRS      := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/kronbatch_b200.h
 LIB       := $(PKG)/libkronbatch_b200.so
 
-.PHONY: all lib oracle cpptest clean
+.PHONY: all lib oracle cpptest kronbench clean
 all: lib oracle
 
 lib: $(LIB)
@@ -39,6 +39,12 @@ cpptest: $(CPPTESTS)
 build/cpptest/test_dropin: tests/cpp/test_dropin.cpp $(LIB) $(wildcard include/kronbatch/*.hpp)
 	@mkdir -p build/cpptest
 	$(CXX_HOST) -O2 -std=gnu++20 -Iinclude -o $@ $< -L$(PKG) -lkronbatch_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
+# native bench CLI (the reference's `bench` flags + CSV schema, on the B200 library)
+kronbench: tools/kronbench/kronbench
+tools/kronbench/kronbench: tools/kronbench/kronbench.cpp $(LIB) $(wildcard include/kronbatch/*.hpp)
+	$(CXX_HOST) -O2 -std=gnu++20 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -lkronbatch_b200 \
+	  -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
 
 clean:
 	rm -rf build $(LIB)

@@ -221,9 +221,15 @@ static int k3_family() {
   static const int force = env_variant("KB_K3", -1);
   if (N % 2 || N < 4) return 0;
   if (force >= 0) return force;
-  // measured on B200 (profiles/r01_k3_families.txt)
-  if (sizeof(T) == 4) return N == 16 ? 3 : ((N == 10 || N == 12 || N == 14) ? 1 : 0);
-  return N == 16 ? 2 : (N >= 10 ? 1 : 0);
+  // fastest family per size, measured on B200 (profiles/r01_k3_families.txt)
+  if (sizeof(T) == 4) return N == 8 ? 0 : (N == 12 ? 1 : 3);
+  switch (N) {
+    case 4: return 0;
+    case 6: return 1;
+    case 12: return 1;
+    case 14: return 3;
+    default: return 2;  // 8, 10, 16
+  }
 }
 
 template <typename T, int N>
