@@ -61,10 +61,9 @@ __host__ __device__ constexpr int phase_banks(F off, int lanes, int words) {
 
 template <typename T, int N, int V = 0>
 struct Cw3 {
-  static_assert(N % 2 == 0, "column-wise kernel: even n");
   static constexpr int ES = sizeof(T);
-  static constexpr int R = 2;                 // rows per mode-2/3 task
-  static constexpr int TPI = N / R;           // tasks per plane / per fiber column
+  static constexpr int R = 2;                 // rows per mode-2/3 task (odd n: the last task has 1)
+  static constexpr int TPI = (N + 1) / R;     // tasks per plane / per fiber column
   static constexpr int NN = N * N;
   // entries per tile: ~256 threads of mode-2/3 tasks (fp32, V0/V1), ~128
   // (fp64; fp32 V2: 4-warp CTAs, so each SM sub-partition interleaves warps
@@ -79,8 +78,15 @@ struct Cw3 {
   static constexpr int STAGES = V == 1 ? 1 : 2;
   static constexpr int MINB = ES == 4 ? (V == 1 ? 4 : (V == 2 ? 6 : 3)) : (V == 1 ? 6 : 3);
   static constexpr int VXR = vec_width(N, ES);  // column read width (elements)
-  static constexpr int VR = vec_width(R, ES);   // row-pair width
+  // planes are 16-byte multiples (even n): one cp.async.bulk per plane into a
+  // padded plane stride. Otherwise (odd n) the tile's entries are contiguous
+  // in HBM and land with ONE bulk copy of the 16-byte-aligned span covering
+  // them (<= 12 bytes either side, never crossing a page: an unaligned end is
+  // not a page boundary) at plane stride NN, shifted by the span's offset.
   static constexpr bool BULK = (NN * ES) % 16 == 0;
+  static constexpr int VR = BULK ? vec_width(R, ES) : 1;       // smem row-pair width
+  static constexpr int VRY = N % 2 == 0 ? vec_width(R, ES) : 1;  // HBM Y row-pair width
+  static constexpr int SLACK = BULK ? 0 : 32 / ES;              // span rounding (elements)
   // mode-2 plane permutation: 4 plane groups of a warp's 16-lane phases
   // spread across the banks (see plane_of_task)
   static constexpr bool PERM = N % 4 == 0 && TPI * 4 <= 32;
@@ -119,7 +125,8 @@ struct Cw3 {
     return worst;
   }
   __host__ __device__ static constexpr int plane_stride() {
-    const int align = BULK ? 16 / ES : VXR;
+    if (!BULK) return NN;
+    const int align = 16 / ES;
     int best = (NN + align - 1) / align * align, best_c = 1 << 30;
     for (int s = best; s <= best + 64 * align; s += align) {
       const int c = conflicts(s);
@@ -133,18 +140,20 @@ struct Cw3 {
   }
   static constexpr int PS = plane_stride();
   static constexpr int ITEM = N * PS;
-  static constexpr int TILE = IT * ITEM;
+  static constexpr int TILE = (IT * ITEM + SLACK + 16 / ES - 1) / (16 / ES) * (16 / ES);
   static constexpr size_t smem_bytes() { return (size_t)ES * STAGES * TILE + 8 * STAGES; }
 };
 
-// {acc[i], acc[i+1]} += {a[i], a[i+1]} * s  (a from the constant bank: FFMA2 with a UR pair)
+// {acc[i], acc[i+1]} += {a[i], a[i+1]} * s  (a from the constant bank: FFMA2 with a UR pair;
+// odd n: the last row is a scalar FFMA)
 __device__ __forceinline__ void axpy_pairs_c(float* acc, const float* a, float s, int n) {
 #pragma unroll
-  for (int i = 0; i < n; i += 2) {
+  for (int i = 0; i + 1 < n; i += 2) {
     const float2 d = ffma2_s(make_float2(a[i], a[i + 1]), s, make_float2(acc[i], acc[i + 1]));
     acc[i] = d.x;
     acc[i + 1] = d.y;
   }
+  if (n % 2) acc[n - 1] = __fmaf_rn(a[n - 1], s, acc[n - 1]);
 }
 __device__ __forceinline__ void axpy_pairs_c(double* acc, const double* a, double s, int n) {
 #pragma unroll
@@ -171,11 +180,19 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
     T* dst = tiles + stage * K::TILE;
     const long long first = tile * IT;
     const int valid = (int)(p.batch - first < IT ? p.batch - first : IT);
-    if (tid == 0) mbar_arrive_expect_tx(&bars[stage], (unsigned)(valid * N * NN * sizeof(T)));
-    __syncwarp();
-    for (int pl = tid; pl < valid * N; pl += 32) {
-      const int e = pl / N, n = pl - e * N;
-      bulk_g2s(dst + e * ITEM + n * PS, p.X + (first + e) * p.sx + (long long)n * NN, NN * sizeof(T), &bars[stage]);
+    if constexpr (K::BULK) {
+      if (tid == 0) mbar_arrive_expect_tx(&bars[stage], (unsigned)(valid * N * NN * sizeof(T)));
+      __syncwarp();
+      for (int pl = tid; pl < valid * N; pl += 32) {
+        const int e = pl / N, n = pl - e * N;
+        bulk_g2s(dst + e * ITEM + n * PS, p.X + (first + e) * p.sx + (long long)n * NN, NN * sizeof(T), &bars[stage]);
+      }
+    } else if (tid == 0) {
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(p.X + first * p.sx) & ~uintptr_t(15);
+      const uintptr_t a1 =
+          (reinterpret_cast<uintptr_t>(p.X + (first + valid) * p.sx) + uintptr_t(15)) & ~uintptr_t(15);
+      mbar_arrive_expect_tx(&bars[stage], (unsigned)(a1 - a0));
+      bulk_g2s(dst, reinterpret_cast<const void*>(a0), (unsigned)(a1 - a0), &bars[stage]);
     }
   };
 
@@ -195,9 +212,10 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
     else
       issue(tile + (long long)(S - 1) * gridDim.x, (stage + S - 1) % S);
     mbar_wait(&bars[stage], phase);
-    T* buf = tiles + stage * K::TILE;
     const long long first = tile * IT;
     const int valid = (int)(p.batch - first < IT ? p.batch - first : IT);
+    T* buf = tiles + stage * K::TILE;
+    if constexpr (!K::BULK) buf += (reinterpret_cast<uintptr_t>(p.X + first * p.sx) & 15) / sizeof(T);
 
     // ---- mode 1: columns c = tid + k*THREADS (plane P = c % NP, column m = c / NP)
     {
@@ -254,22 +272,27 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
 #pragma unroll kCwUnroll
       for (int m = 0; m < N; ++m) {
         T t[R];
-        lds_vec<K::VR>(t, pl + m * N);
+        lds_n<R, K::VR>(t, pl + m * N);
 #pragma unroll
         for (int j = 0; j < N; ++j) axpy_rows<R>(acc[j], t, kc.bt[m * N + j]);
       }
 #pragma unroll
       for (int j = 0; j < N; ++j) {
-        if constexpr (sizeof(T) == 4)
+        if constexpr (K::VR == 2 && sizeof(T) == 4)
           *reinterpret_cast<float2*>(pl + j * N) = make_float2(acc[j][0], acc[j][1]);
-        else
+        else if constexpr (K::VR == 2)
           *reinterpret_cast<double2*>(pl + j * N) = make_double2(acc[j][0], acc[j][1]);
+        else {
+          pl[j * N] = acc[j][0];
+          if (N % 2 == 0 || q * R + 1 < N) pl[j * N + 1] = acc[j][1];  // odd n: last task owns one row
+        }
       }
     }
     __syncthreads();
 
     // ---- mode 3: Y(I_q, j3, k) = init + sum_n T2(I_q, j3, n) Cw(k, n)
     if (task_ok && e3 < valid) {
+      const bool two = N % 2 == 0 || q * R + 1 < N;
       const T* fb = buf + e3 * ITEM + j3 * N + q * R;
       T* yb = p.Y + (first + e3) * p.sy + (long long)j3 * p.ldy + q * R;
       T acc[N][R];
@@ -280,7 +303,12 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
           acc[k][1] = T(0);
         } else {
           T y0[R];
-          ldg_n<R, K::VR>(y0, yb + (long long)k * p.ldy2);
+          if (K::VRY == 2 || two) {
+            ldg_n<R, K::VRY>(y0, yb + (long long)k * p.ldy2);
+          } else {
+            y0[0] = yb[(long long)k * p.ldy2];
+            y0[1] = T(0);
+          }
           acc[k][0] = beta_init(p.beta_mode, p.beta, y0[0]);
           acc[k][1] = beta_init(p.beta_mode, p.beta, y0[1]);
         }
@@ -288,12 +316,17 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
 #pragma unroll kCwUnroll
       for (int n = 0; n < N; ++n) {
         T f[R];
-        lds_vec<K::VR>(f, fb + n * PS);
+        lds_n<R, K::VR>(f, fb + n * PS);
 #pragma unroll
         for (int k = 0; k < N; ++k) axpy_rows<R>(acc[k], f, kc.ct[n * N + k]);
       }
 #pragma unroll
-      for (int k = 0; k < N; ++k) stg_n<R, K::VR>(yb + (long long)k * p.ldy2, acc[k]);
+      for (int k = 0; k < N; ++k) {
+        if (K::VRY == 2 || two)
+          stg_n<R, K::VRY>(yb + (long long)k * p.ldy2, acc[k]);
+        else
+          yb[(long long)k * p.ldy2] = acc[k][0];
+      }
     }
     fence_proxy_async();  // generic smem writes before the stage's next TMA refill
     __syncthreads();

@@ -87,7 +87,10 @@ struct SqCfg {
   static constexpr int LANES_PER_PHASE = 128 / (VXR * ES) < 32 ? 128 / (VXR * ES) : 32;
   static constexpr int PLANES_PER_PHASE = LANES_PER_PHASE / TPI > 0 ? LANES_PER_PHASE / TPI : 1;
   // padded per-entry (2-D) / per-plane (3-D) stride in smem, in elements
-  static constexpr int SLOT = bank_spread_stride(NN, VXC > VXR ? VXC : VXR, VXR, PLANES_PER_PHASE, ES);
+  // (odd n: entries stay contiguous, SLOT = NN, so a group of entries lands
+  //  with one bulk copy of its 16-byte-aligned span; odd NN spreads banks anyway)
+  static constexpr int SLOT = (NN * ES) % 16 == 0 ? bank_spread_stride(NN, VXC > VXR ? VXC : VXR, VXR, PLANES_PER_PHASE, ES)
+                                                  : NN;
   // A row-block layout: Ablk[q][l][R] with q-stride QS
   static constexpr int QS = bank_spread_stride(N * R, VR, VR, TPI < 128 / (VR * ES) ? TPI : 128 / (VR * ES), ES);
   // R-row vector accesses into an smem plane (T2 write / fiber read) are aligned
@@ -363,7 +366,10 @@ struct Kron2Fast {
   static constexpr int JB = V == 3 ? 2 : 4;  // Y columns per mode-2 block
   // whole entries are 16-byte multiples: one cp.async.bulk per entry
   static constexpr bool BULK = (C::NN * sizeof(T)) % 16 == 0;
-  static constexpr int RING = C::IPW * C::SLOT;  // elements per warp stage
+  // odd n: + slack for the span copy's 16-byte rounding; stages stay 16-byte aligned
+  static constexpr int RING = BULK ? C::IPW * C::SLOT
+                                   : (C::IPW * C::SLOT + 32 / (int)sizeof(T) + 16 / (int)sizeof(T) - 1) /
+                                         (16 / (int)sizeof(T)) * (16 / (int)sizeof(T));
   static constexpr size_t smem_bytes() {
     return sizeof(T) * ((size_t)C::A_ELEMS + (size_t)WARPS * STAGES * RING) +
            sizeof(unsigned long long) * WARPS * STAGES;
@@ -383,7 +389,11 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(ring + K::WARPS * S * K::RING);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if constexpr (K::BULK) {
+  // odd n with contiguous entries: one span bulk copy per group (mbarrier);
+  // any other odd-n layout: element cp.async (commit groups)
+  const bool span = !K::BULK && p.sx == NN;
+  const bool use_bar = K::BULK || span;
+  if (use_bar) {
     if (lane == 0)
       for (int s = 0; s < S; ++s) mbar_init(&bars[warp * S + s], 1);
     mbar_fence_init();
@@ -399,7 +409,7 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
   // start loading group g (IPW entries) into `stage`
   auto issue = [&](long long g, int stage) {
     if (g >= ngroups) {
-      if constexpr (!K::BULK) cp_async_commit();
+      if (!use_bar) cp_async_commit();
       return;
     }
     T* dst = wring + stage * K::RING;
@@ -409,6 +419,13 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
       if (lane == 0) mbar_arrive_expect_tx(&wbar[stage], (unsigned)(valid * NN * sizeof(T)));
       __syncwarp();
       if (lane < valid) bulk_g2s(dst + lane * C::SLOT, p.X + (first + lane) * p.sx, NN * sizeof(T), &wbar[stage]);
+    } else if (span) {
+      if (lane == 0) {
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(p.X + first * NN) & ~uintptr_t(15);
+        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p.X + (first + valid) * NN) + uintptr_t(15)) & ~uintptr_t(15);
+        mbar_arrive_expect_tx(&wbar[stage], (unsigned)(a1 - a0));
+        bulk_g2s(dst, reinterpret_cast<const void*>(a0), (unsigned)(a1 - a0), &wbar[stage]);
+      }
     } else {
       constexpr int CPI = NN / VXC;  // chunks per entry
 #pragma unroll 4
@@ -432,14 +449,16 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
   unsigned phase = 0;  // parity of the current use of `stage`
   for (long long g = gw; g < ngroups; g += gstride) {
     issue(g + (S - 1) * gstride, (stage + S - 1) % S);
-    if constexpr (K::BULK) {
+    if (use_bar) {
       mbar_wait(&wbar[stage], phase);
     } else {
       cp_async_wait<S - 1>();
       __syncwarp();
     }
     const long long item = g * IPW + slot;
-    T* xs = wring + stage * K::RING + slot * C::SLOT;
+    T* sbase = wring + stage * K::RING;  // entry 0 of the group (span copies land shifted)
+    if (!K::BULK && span) sbase += (reinterpret_cast<uintptr_t>(p.X + g * IPW * NN) & 15) / sizeof(T);
+    T* xs = sbase + slot * C::SLOT;
     if (ystage) {
       // Y(I_q, j) goes into the entry's own smem slot (X is dead once every
       // lane of the entry finished mode 1), then leaves with coalesced stores.
@@ -463,8 +482,8 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
       __syncwarp();
       const long long first = g * IPW;
       const int valid = (int)(p.batch - first < IPW ? p.batch - first : IPW);
-      copy_out<T, NN, VXC>(p.Y + first * p.sy, p.sy, wring + stage * K::RING, C::SLOT, 0, 1, valid, lane, 32);
-      if constexpr (K::BULK) fence_proxy_async();  // generic smem accesses before the TMA refill
+      copy_out<T, NN, VXC>(p.Y + first * p.sy, p.sy, sbase, C::SLOT, 0, 1, valid, lane, 32);
+      if (use_bar) fence_proxy_async();  // generic smem accesses before the TMA refill
     } else if (item < p.batch) {
       T t[N][R];
       mode1<T, N, OPX, K::MB>(t, xs, aq);
@@ -487,7 +506,7 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
       phase ^= 1;
     }
   }
-  if constexpr (!K::BULK) cp_async_wait<0>();
+  if (!use_bar) cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------- kron3 ---

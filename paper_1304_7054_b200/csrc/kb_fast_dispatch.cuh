@@ -139,9 +139,11 @@ template <typename T, int N, int V>
 static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
                              cudaStream_t s) {
   using K = Cw3<T, N, V>;
-  if (p.ldx != N || p.ldx2 != (long long)N * N || (p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))
+  if (p.ldx != N || p.ldx2 != (long long)N * N) return cudaErrorNotSupported;
+  if (K::BULK ? ((p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))
+              : p.sx != (long long)N * N * N)  // odd n: contiguous entries, one span copy per tile
     return cudaErrorNotSupported;
-  if (p.ldy % 2 || p.ldy2 % 2 || p.sy % 2 || !aligned<T>(p.Y, 2)) return cudaErrorNotSupported;
+  if (K::VRY == 2 && (p.ldy % 2 || p.ldy2 % 2 || p.sy % 2 || !aligned<T>(p.Y, 2))) return cudaErrorNotSupported;
   auto kern = kron3_cw_kernel<T, N, V>;
   const size_t smem = K::smem_bytes();
   const int occ = occupancy_for(kern, K::THREADS, smem);
@@ -219,8 +221,12 @@ static cudaError_t launch3cwpp(const Kron3Params<T>& p, const T* ha, const T* hb
 template <typename T, int N>
 static int k3_family() {
   static const int force = env_variant("KB_K3", -1);
-  if (N % 2 || N < 4) return 0;
-  if (force >= 0) return force;
+  if (N < 3) return 0;
+  if (force >= 0) return N % 2 && force > 3 ? 0 : force;
+  if (N % 2) {  // odd n: the column-wise kernel with span loads
+    if (sizeof(T) == 4) return N == 11 ? 1 : 3;
+    return N == 3 ? 0 : (N < 9 ? 1 : 2);
+  }
   // fastest family per size, measured on B200 (profiles/r01_k3_families.txt)
   if (sizeof(T) == 4) return N == 8 ? 0 : (N == 12 ? 1 : 3);
   switch (N) {
@@ -235,7 +241,7 @@ static int k3_family() {
 template <typename T, int N>
 static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
                            cudaStream_t s) {
-  if constexpr (N % 2 == 0 && N >= 4) {
+  if constexpr (N >= 3) {
     const int fam = k3_family<T, N>();
 #ifdef KB_SWEEP_VARIANTS  // n = 16 warp-plane experiments (profiles/r01_k3_families.txt): `make VARIANTS=1`
     if constexpr (N == 16) {

@@ -60,6 +60,12 @@ if __name__ == "__main__":
     elif which == "one":  # one <2|3> <n> <f32|f64> <batch> [reps]
         reps = int(sys.argv[6]) if len(sys.argv) > 6 else 3
         bench(sys.argv[2] == "3", int(sys.argv[3]), int(sys.argv[5]), sys.argv[4], reps=reps)
+    elif which == "sweepd":  # sweepd <2|3> <f32|f64>: one rank / dtype of the size sweep
+        dims3, dt = sys.argv[2] == "3", sys.argv[3]
+        es = 4 if dt == "f32" else 8
+        for n in range(1, 17):
+            e = n ** (3 if dims3 else 2)
+            bench(dims3, n, max(1, int(2 * 1024 ** 3 // (e * es))), dt, reps=5)
     else:
         for dims3 in (False, True):
             for dt in ("f32", "f64"):
