@@ -8,6 +8,7 @@
 #include <map>
 #include <utility>
 
+#include "kb_cw2.cuh"
 #include "kb_cw3.cuh"
 #include "kb_fast.cuh"
 #include "kb_kernels.h"
@@ -51,9 +52,9 @@ static int env_variant(const char* name, int dflt = 0) {
 }
 
 // Stage Y through shared memory + coalesced copy-out instead of the direct
-// R-row stores. Measured per size on B200 (profiles/r01_sweep_ystage.txt):
-// it pays for 2-D where the row-block stores are narrow and scattered
-// (fp32 n = 5, 6, 7, 9, 10, 14; fp64 n = 3, 5, 6, 7) and loses everywhere
+// R-row stores. Measured per size on B200 (profiles/r01_sweep_ystage.txt, r01_sweep2_span.txt):
+// it pays for 2-D wherever the row-block stores are narrow or scattered
+// (fp32: all n but 1, 2, 4, 8, 16; fp64: n = 3..8, 12) and loses everywhere
 // else, including every 3-D case (the extra CTA barrier costs more than the
 // store coalescing gains). KB_YSTAGE=0 / 1 forces it off / on for sweeps.
 template <typename T, int N, int DIMS>
@@ -62,8 +63,8 @@ static bool want_ystage(bool legal) {
   if (!legal) return false;
   if (force >= 0) return force != 0;
   if (DIMS == 3) return false;
-  if (sizeof(T) == 4) return N == 5 || N == 6 || N == 7 || N == 9 || N == 10 || N == 14;
-  return N == 3 || N == 5 || N == 6 || N == 7;
+  if (sizeof(T) == 4) return !(N <= 2 || N == 4 || N == 8 || N == 16);
+  return (N >= 3 && N <= 8) || N == 12;
 }
 
 template <typename T, int N, int OPX, int V>
@@ -91,8 +92,58 @@ static cudaError_t launch2v(const Kron2Params<T>& p, const T* ha, const T* hw, i
   return cudaGetLastError();
 }
 
+// Column-wise 2-D kernel (kb_cw2.cuh), op_x = N. ys: Y staged through smem.
+template <typename T, int N>
+static cudaError_t launch2cw(const Kron2Params<T>& p, const T* ha, const T* hw, int sm_count, cudaStream_t s,
+                             bool ys) {
+  using K = Cw2<T, N>;
+  if (p.opx || p.ldx != N) return cudaErrorNotSupported;
+  if (K::BULK ? ((p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T))) : p.sx != (long long)N * N)
+    return cudaErrorNotSupported;
+  if (ys) {
+    constexpr int vc = K::BULK ? K::VXC : 1;
+    if (p.ldy != N || p.sy % vc || !aligned<T>(p.Y, vc)) ys = false;
+  }
+  if (!ys && K::VRY == 2 && (p.ldy % 2 || p.sy % 2 || !aligned<T>(p.Y, 2))) return cudaErrorNotSupported;
+  auto kern = kron2_cw_kernel<T, N>;
+  const int threads = K::WARPS * 32;
+  const size_t smem = K::smem_bytes();
+  const int occ = occupancy_for(kern, threads, smem);
+  if (occ <= 0) return cudaErrorNotSupported;
+  const long long ngroups = (p.batch + K::EPW - 1) / K::EPW;
+  const long long want = (ngroups + K::WARPS - 1) / K::WARPS;
+  const int grid = (int)(want < (long long)sm_count * occ ? want : (long long)sm_count * occ);
+  SqConsts2<T, N> kc;
+  for (int i = 0; i < N * N; ++i) {
+    kc.a[i] = ha[i];
+    kc.w[i] = hw[i];
+  }
+  kern<<<grid, threads, smem, s>>>(p, kc, ngroups, ys ? 1 : 0);
+  return cudaGetLastError();
+}
+
+// 2-D kernel family per size: 0 = row-owner kron2_sq_kernel, 1 = column-wise
+// with direct Y stores, 2 = column-wise with Y staged through smem. KB_K2
+// overrides the default for sweeps.
+template <typename T, int N>
+static int k2_family() {
+  static const int force = env_variant("KB_K2", -1);
+  if (force >= 0) return force;
+  // fastest family per size, measured on B200 (profiles/r01_k2_families.txt)
+  if (sizeof(T) == 4) return (N == 1 || N == 5 || (N >= 9 && N <= 13) || N == 15) ? 1 : 0;
+  if (N == 3 || N == 8) return 2;
+  return (N == 1 || (N >= 9 && N <= 11) || N == 13 || N == 14) ? 1 : 0;
+}
+
 template <typename T, int N, int OPX>
 static cudaError_t launch2(const Kron2Params<T>& p, const T* ha, const T* hw, int sm_count, cudaStream_t s) {
+  if constexpr (OPX == 0) {
+    const int fam = k2_family<T, N>();
+    if (fam == 1 || fam == 2) {
+      const cudaError_t e = launch2cw<T, N>(p, ha, hw, sm_count, s, fam == 2);
+      if (e != cudaErrorNotSupported) return e;
+    }
+  }
 #ifdef KB_SWEEP_VARIANTS  // tuning variants: built only with `make VARIANTS=1`
   if constexpr (N == 10 || N == 16) {
     static const int v = env_variant("KB_VARIANT2");
