@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import threading
 from dataclasses import dataclass, field
 from typing import Any, Optional, Sequence
 
@@ -61,21 +62,38 @@ def is_transposed(op: MatrixOp) -> bool:
 
 # ----------------------------------------------------------------- buffers --
 
+_TORCH = None
+
+
+def _torch():
+    """torch, imported once (False when absent); the per-call path must not re-import."""
+    global _TORCH
+    if _TORCH is None:
+        try:
+            import torch
+
+            _TORCH = torch
+        except ImportError:  # pragma: no cover
+            _TORCH = False
+    return _TORCH
+
+
 def _buf_info(data):
     """(address, numel, dtype-name) of a flat buffer; None -> (0, 0, None)."""
     if data is None:
         return 0, 0, None
-    try:
-        import torch
-
-        if isinstance(data, torch.Tensor):
-            if data.dtype not in (torch.float32, torch.float64):
-                raise TypeError(f"unsupported element type {data.dtype}: float32 or float64 only")
-            if not data.is_contiguous():
-                raise TypeError("buffer tensors must be contiguous (describe strides with ld / batch_stride)")
-            return data.data_ptr(), data.numel(), "float32" if data.dtype == torch.float32 else "float64"
-    except ImportError:  # pragma: no cover
-        pass
+    torch = _torch()
+    if torch and isinstance(data, torch.Tensor):
+        dt = data.dtype
+        if dt is torch.float32:
+            name = "float32"
+        elif dt is torch.float64:
+            name = "float64"
+        else:
+            raise TypeError(f"unsupported element type {data.dtype}: float32 or float64 only")
+        if not data.is_contiguous():
+            raise TypeError("buffer tensors must be contiguous (describe strides with ld / batch_stride)")
+        return data.data_ptr(), data.numel(), name
     if isinstance(data, np.ndarray):
         if data.dtype not in (np.float32, np.float64):
             raise TypeError(f"unsupported element type {data.dtype}: float32 or float64 only")
@@ -266,6 +284,16 @@ class Exec:
     tf32: bool = False  # allow the tcgen05 3xTF32 kernel (fp32 kron3, n = 16): 1e-5 parity, not bit-exact
 
     def to_c(self):
+        """(kb_exec struct, keep-alive) -- cached while the fields are unchanged."""
+        key = (tuple(self.devices), self.stream, self.asynchronous, self.tf32)
+        cached = self.__dict__.get("_c_cache")
+        if cached is not None and cached[0] == key:
+            return cached[1], cached[2]
+        ex, arr = self._build_c()
+        self.__dict__["_c_cache"] = (key, ex, arr)
+        return ex, arr
+
+    def _build_c(self):
         arr = (C.c_int32 * max(1, len(self.devices)))(*self.devices) if self.devices else None
         s = self.stream
         if s is not None and hasattr(s, "cuda_stream"):
@@ -282,16 +310,37 @@ def _ptr_of(view):
     return (addr + view.offset * esz) if addr else 0, dt
 
 
-def _common_dtype(*views):
-    dts = {(_buf_info(v.data)[2]) for v in views if v is not None and v.data is not None}
-    dts.discard(None)
+def _ptrs_and_dtype(*views):
+    """Element-0 addresses of the views' buffers (0 for none) and their common
+    element type -- one _buf_info per buffer."""
+    ptrs, dts = [], set()
+    for v in views:
+        addr, _, dt = _buf_info(v.data)
+        if dt is not None:
+            dts.add(dt)
+        ptrs.append((addr + v.offset * (4 if dt == "float32" else 8)) if addr else 0)
     if len(dts) > 1:
         raise TypeError("all buffers in a kernel call share one element type (float32 or float64)")
-    return dts.pop() if dts else "float64"
+    return ptrs, (dts.pop() if dts else "float64")
+
+
+def _common_dtype(*views):
+    return _ptrs_and_dtype(*[v for v in views if v is not None])[1]
+
+
+_OPCODE = {MatrixOp.NoTranspose: b"N", MatrixOp.Transpose: b"T", MatrixOp.ConjTranspose: b"C"}
+_ERR = threading.local()
+
+
+def _opc(op) -> bytes:
+    code = _OPCODE.get(op)
+    return code if code is not None else _OPCODE[MatrixOp(op)]
 
 
 def _call(fn, *args, exec_: Optional[Exec] = None):
-    err = C.create_string_buffer(1024)
+    err = getattr(_ERR, "buf", None)
+    if err is None:
+        err = _ERR.buf = C.create_string_buffer(1024)
     ex_ptr = None
     keep = None
     if exec_ is not None:
@@ -299,7 +348,8 @@ def _call(fn, *args, exec_: Optional[Exec] = None):
         ex_ptr = C.byref(ex)
     rc = fn(*args, ex_ptr, err, 1024)
     del keep
-    _lib.raise_for(rc, err)
+    if rc:
+        _lib.raise_for(rc, err)
 
 
 def kron2(pr: KronProblem2D, a: MatrixView, b: MatrixView, x: BatchView, y: BatchView,
@@ -311,23 +361,19 @@ def kron2(pr: KronProblem2D, a: MatrixView, b: MatrixView, x: BatchView, y: Batc
     validate_batch(y, "kron2: Y")
     ra, ca = op_dims(pr.op_a, a.rows, a.cols)
     rb, cb = op_dims(pr.op_b, b.rows, b.cols)
-    _require(ra == pr.m_a and ca == pr.n_a, "kron2: A",
-             f"op(A) is {_dim2s(ra, ca)}, expected {_dim2s(pr.m_a, pr.n_a)}")
-    _require(rb == pr.m_b and cb == pr.n_b, "kron2: B",
-             f"op(B) is {_dim2s(rb, cb)}, expected {_dim2s(pr.m_b, pr.n_b)}")
+    if not (ra == pr.m_a and ca == pr.n_a):
+        _layout_error("kron2: A", f"op(A) is {_dim2s(ra, ca)}, expected {_dim2s(pr.m_a, pr.n_a)}")
+    if not (rb == pr.m_b and cb == pr.n_b):
+        _layout_error("kron2: B", f"op(B) is {_dim2s(rb, cb)}, expected {_dim2s(pr.m_b, pr.n_b)}")
     _require(x.batch_count == y.batch_count, "kron2", "X and Y batch_count differ")
     rx, cx = op_dims(pr.op_x, x.base.rows, x.base.cols)
-    _require(rx == pr.n_a and cx == pr.n_b, "kron2: X",
-             f"op(X) is {_dim2s(rx, cx)}, expected {_dim2s(pr.n_a, pr.n_b)}")
-    _require(y.base.rows == pr.m_a and y.base.cols == pr.m_b, "kron2: Y",
-             f"entry is {_dim2s(y.base.rows, y.base.cols)}, expected {_dim2s(pr.m_a, pr.m_b)}")
-    dt = _common_dtype(a, b, x.base, y.base)
+    if not (rx == pr.n_a and cx == pr.n_b):
+        _layout_error("kron2: X", f"op(X) is {_dim2s(rx, cx)}, expected {_dim2s(pr.n_a, pr.n_b)}")
+    if not (y.base.rows == pr.m_a and y.base.cols == pr.m_b):
+        _layout_error("kron2: Y", f"entry is {_dim2s(y.base.rows, y.base.cols)}, expected {_dim2s(pr.m_a, pr.m_b)}")
+    (pa, pb, px, py), dt = _ptrs_and_dtype(a, b, x.base, y.base)
     fn = _lib.lib.kb_skron2 if dt == "float32" else _lib.lib.kb_dkron2
-    pa, _ = _ptr_of(a)
-    pb, _ = _ptr_of(b)
-    px, _ = _ptr_of(x.base)
-    py, _ = _ptr_of(y.base)
-    _call(fn, MatrixOp(pr.op_a).value.encode(), MatrixOp(pr.op_b).value.encode(), MatrixOp(pr.op_x).value.encode(),
+    _call(fn, _opc(pr.op_a), _opc(pr.op_b), _opc(pr.op_x),
           pr.m_a, pr.n_a, pr.m_b, pr.n_b, x.batch_count, pr.alpha, pa or None, a.ld, a.len, pb or None, b.ld, b.len,
           px or None, x.base.ld, x.batch_stride, x.base.len, pr.beta, py or None, y.base.ld, y.batch_stride,
           y.base.len, exec_=exec_)
@@ -344,26 +390,21 @@ def kron3(pr: KronProblem3D, a: MatrixView, b: MatrixView, c: MatrixView, x: Bat
     ra, ca = op_dims(pr.op_a, a.rows, a.cols)
     rb, cb = op_dims(pr.op_b, b.rows, b.cols)
     rc, cc = op_dims(pr.op_c, c.rows, c.cols)
-    _require(ra == pr.m_a and ca == pr.n_a, "kron3: A",
-             f"op(A) is {_dim2s(ra, ca)}, expected {_dim2s(pr.m_a, pr.n_a)}")
-    _require(rb == pr.m_b and cb == pr.n_b, "kron3: B",
-             f"op(B) is {_dim2s(rb, cb)}, expected {_dim2s(pr.m_b, pr.n_b)}")
-    _require(rc == pr.m_c and cc == pr.n_c, "kron3: C",
-             f"op(C) is {_dim2s(rc, cc)}, expected {_dim2s(pr.m_c, pr.n_c)}")
+    if not (ra == pr.m_a and ca == pr.n_a):
+        _layout_error("kron3: A", f"op(A) is {_dim2s(ra, ca)}, expected {_dim2s(pr.m_a, pr.n_a)}")
+    if not (rb == pr.m_b and cb == pr.n_b):
+        _layout_error("kron3: B", f"op(B) is {_dim2s(rb, cb)}, expected {_dim2s(pr.m_b, pr.n_b)}")
+    if not (rc == pr.m_c and cc == pr.n_c):
+        _layout_error("kron3: C", f"op(C) is {_dim2s(rc, cc)}, expected {_dim2s(pr.m_c, pr.n_c)}")
     _require(x.batch_count == y.batch_count, "kron3", "X and Y batch_count differ")
     _require(x.base.dim1 == pr.n_a and x.base.dim2 == pr.n_b and x.base.dim3 == pr.n_c, "kron3: X",
              "entry dims do not match n_a x n_b x n_c")
     _require(y.base.dim1 == pr.m_a and y.base.dim2 == pr.m_b and y.base.dim3 == pr.m_c, "kron3: Y",
              "entry dims do not match m_a x m_b x m_c")
-    dt = _common_dtype(a, b, c, x.base, y.base)
+    (pa, pb, pc, px, py), dt = _ptrs_and_dtype(a, b, c, x.base, y.base)
     fn = _lib.lib.kb_skron3 if dt == "float32" else _lib.lib.kb_dkron3
-    pa, _ = _ptr_of(a)
-    pb, _ = _ptr_of(b)
-    pc, _ = _ptr_of(c)
-    px, _ = _ptr_of(x.base)
-    py, _ = _ptr_of(y.base)
     wp = _buf_info(work.data)[0] if work.data is not None else 0
-    _call(fn, MatrixOp(pr.op_a).value.encode(), MatrixOp(pr.op_b).value.encode(), MatrixOp(pr.op_c).value.encode(),
+    _call(fn, _opc(pr.op_a), _opc(pr.op_b), _opc(pr.op_c),
           pr.m_a, pr.n_a, pr.m_b, pr.n_b, pr.m_c, pr.n_c, x.batch_count, pr.alpha, pa or None, a.ld, a.len,
           pb or None, b.ld, b.len, pc or None, c.ld, c.len, px or None, x.base.ld, x.base.ld2, x.batch_stride,
           x.base.len, pr.beta, py or None, y.base.ld, y.base.ld2, y.batch_stride, y.base.len, wp or None,
