@@ -29,15 +29,20 @@ struct Cw2 {
   static constexpr int ES = sizeof(T);
   static constexpr int R = 2;
   static constexpr int TPI = (N + 1) / 2;          // mode-2 tasks per entry
-  static constexpr int EPW = 32 / TPI;             // entries per warp group
   static constexpr int NN = N * N;
+  // tiny entries (<= 64 B): KE x more entries per group, contiguous in smem,
+  // one span copy per group -- amortises the per-group TMA / mbarrier cost
+  static constexpr bool TINY = NN * ES <= 64;
+  static constexpr int KE = NN * ES <= 16 ? 8 : (TINY ? 2 : 1);
+  static constexpr int EPW = KE * (32 / TPI);      // entries per warp group
   static constexpr int NCOL = EPW * N;             // mode-1 columns per group
   static constexpr int CA = (NCOL + 31) / 32;      // columns per lane
+  static constexpr int KT = (EPW * TPI + 31) / 32;  // mode-2 tasks per lane
   static constexpr int WARPS = 8;
   static constexpr int STAGES = 3;
   static constexpr int VXR = vec_width(N, ES);     // column read width
-  static constexpr bool BULK = (NN * ES) % 16 == 0;
-  static constexpr int VR = BULK ? vec_width(R, ES) : 1;
+  static constexpr bool BULK = (NN * ES) % 16 == 0 && !TINY;  // one bulk copy per entry (else per group span)
+  static constexpr int VR = BULK || (TINY && (NN * ES) % 16 == 0) ? vec_width(R, ES) : 1;
   static constexpr int VRY = N % 2 == 0 ? vec_width(R, ES) : 1;
   static constexpr int VXC = vec_width(NN, ES);    // copy-out chunk
   // slot stride: mode-1 column reads (lane c -> entry c % EPW, column c / EPW)
@@ -60,7 +65,7 @@ struct Cw2 {
     return worst;
   }
   __host__ __device__ static constexpr int slot_stride() {
-    if (!BULK) return NN;
+    if (!BULK) return NN;  // odd n / tiny: entries contiguous as in HBM
     const int align = 16 / ES;
     int best = NN, best_c = 1 << 30;
     for (int s = NN; s <= NN + 32 * align; s += align) {
@@ -118,10 +123,6 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) issue(gw + s * gstride, s);
 
-  // mode-2 task of this lane: entry e2, rows 2*q .. 2*q+1 (odd n: the last task owns one)
-  const int e2 = lane / TPI, q = lane % TPI;
-  const bool task_ok = e2 < EPW;
-  const bool two = N % 2 == 0 || q * R + 1 < N;
   int stage = 0;
   unsigned phase = 0;
   for (long long g = gw; g < ngroups; g += gstride) {
@@ -172,8 +173,14 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
     }
     __syncwarp();
 
-    // ---- mode 2: Y(I_q, j) = init + sum_m tmp(I_q, m) w(j, m)
-    if (task_ok && e2 < valid) {
+    // ---- mode 2: Y(I_q, j) = init + sum_m tmp(I_q, m) w(j, m); task t = lane + 32 kt
+    //      -> entry t / TPI, rows 2 (t % TPI) .. +1 (odd n: the last task owns one)
+#pragma unroll
+    for (int kt = 0; kt < K::KT; ++kt) {
+    const int t = lane + 32 * kt;
+    const int e2 = t / TPI, q = t % TPI;
+    const bool two = N % 2 == 0 || q * R + 1 < N;
+    if (e2 < EPW && e2 < valid) {
       T* tr = base + e2 * SLOT + q * R;
       T* yb = p.Y + (first + e2) * p.sy + q * R;
       T acc[N][R];
@@ -222,9 +229,10 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
         }
       }
     }
+    }
     if (ystage) {
       __syncwarp();
-      copy_out<T, NN, (K::BULK ? K::VXC : 1)>(p.Y + first * p.sy, p.sy, base, SLOT, 0, 1, valid, lane, 32);
+      copy_out<T, NN, (K::BULK || K::TINY ? K::VXC : 1)>(p.Y + first * p.sy, p.sy, base, SLOT, 0, 1, valid, lane, 32);
     }
     fence_proxy_async();  // generic smem writes (tmp, staged Y) before the stage's TMA refill
     __syncwarp();

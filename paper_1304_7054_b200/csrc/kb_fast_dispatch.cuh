@@ -100,8 +100,12 @@ static cudaError_t launch2cw(const Kron2Params<T>& p, const T* ha, const T* hw, 
   if (p.opx || p.ldx != N) return cudaErrorNotSupported;
   if (K::BULK ? ((p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T))) : p.sx != (long long)N * N)
     return cudaErrorNotSupported;
+  // tiny entries: groups start 16-byte aligned (EPW * entry bytes is a 16-byte multiple), so vector smem
+  // accesses stay aligned -- needs X itself 16-byte aligned
+  if (K::TINY && ((K::EPW * N * N * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T))))
+    return cudaErrorNotSupported;
   if (ys) {
-    constexpr int vc = K::BULK ? K::VXC : 1;
+    constexpr int vc = K::BULK || K::TINY ? K::VXC : 1;
     if (p.ldy != N || p.sy % vc || !aligned<T>(p.Y, vc)) ys = false;
   }
   if (!ys && K::VRY == 2 && (p.ldy % 2 || p.sy % 2 || !aligned<T>(p.Y, 2))) return cudaErrorNotSupported;
