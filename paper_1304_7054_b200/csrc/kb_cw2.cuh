@@ -133,14 +133,17 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
     T* base = wring + stage * K::RING;
     if constexpr (!K::BULK) base += (reinterpret_cast<uintptr_t>(p.X + first * NN) & 15) / sizeof(T);
 
-    // ---- mode 1: columns c = lane + 32k (entry c % EPW, column c / EPW)
+    // ---- mode 1: columns c = lane + 32k -- padded slots: entry c % EPW, column
+    //      c / EPW (the bank model picked SLOT for this); contiguous entries
+    //      (odd n, tiny): column c of the group, i.e. consecutive lanes read
+    //      consecutive columns
     {
       T acc[K::CA][N];
       T* col[K::CA];
 #pragma unroll
       for (int k = 0; k < K::CA; ++k) {
         const int c = lane + 32 * k;
-        col[k] = base + (c % EPW) * SLOT + (c / EPW) * N;
+        col[k] = K::BULK ? base + (c % EPW) * SLOT + (c / EPW) * N : base + c * N;
 #pragma unroll
         for (int i = 0; i < N; ++i) acc[k][i] = T(0);
       }

@@ -134,9 +134,9 @@ static int k2_family() {
   static const int force = env_variant("KB_K2", -1);
   if (force >= 0) return force;
   // fastest family per size, measured on B200 (profiles/r01_k2_families.txt)
-  if (sizeof(T) == 4) return (N == 1 || N == 5 || (N >= 9 && N <= 13) || N == 15) ? 1 : 0;
+  if (sizeof(T) == 4) return (N <= 5 || (N >= 9 && N <= 13) || N == 15) ? 1 : 0;
   if (N == 3 || N == 8) return 2;
-  return (N == 1 || (N >= 9 && N <= 11) || N == 13 || N == 14) ? 1 : 0;
+  return (N <= 2 || (N >= 9 && N <= 11) || N == 13 || N == 14) ? 1 : 0;
 }
 
 template <typename T, int N, int OPX>
