@@ -12,7 +12,7 @@ endif
 PKG       := paper_1304_7054_b200
 CSRC      := $(PKG)/csrc
 OBJDIR    := build/obj
-SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast_switch.cu $(CSRC)/kb_tc.cu \
+SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast_switch.cu $(CSRC)/kb_tc.cu $(CSRC)/kb_blas.cu \
              $(sort $(wildcard $(CSRC)/kb_sz*.cu))
 OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 HDRS      := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/kronbatch_b200.h

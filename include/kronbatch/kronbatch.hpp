@@ -6,5 +6,7 @@
 
 #include <kronbatch/types.hpp>
 #include <kronbatch/views.hpp>
+#include <kronbatch/kron1.hpp>
 #include <kronbatch/kron2.hpp>
 #include <kronbatch/kron3.hpp>
+#include <kronbatch/gemm_a.hpp>

@@ -16,6 +16,10 @@
  *                             proj/include/kronbatch/kron3.hpp:72-166
  *   kb_kron3_workspace_size <- kronbatch::kron3_workspace_size
  *                             proj/include/kronbatch/kron3.hpp:43-53
+ *   kb_skron1 / kb_dkron1  <- kronbatch::kron1<float|double>
+ *                             proj/include/kronbatch/kron1.hpp:17-62
+ *   kb_sgemm_a / kb_dgemm_a <- kronbatch::gemm_a<float|double>
+ *                             proj/include/kronbatch/gemm_a.hpp:18-76
  *
  * The C++ header include/kronbatch/kronbatch.hpp re-exposes the reference's
  * template API unchanged on top of these.
@@ -104,6 +108,32 @@ int kb_dkron3(char transa, char transb, char transc, int64_t m_a, int64_t n_a, i
               double* Y, int64_t ldy, int64_t ldy2, int64_t ldyp, int64_t leny, double* work,
               int64_t work_capacity, const kb_exec* exec, char* err, size_t errlen);
 
+/* y^p <- alpha * op(A) * x^p + beta * y^p,  p < batch_count (kron1.hpp:9-16),
+ * replaces kronbatch::kron1<float|double> (proj/include/kronbatch/kron1.hpp:17-62).
+ * A is stored m_a x n_a (transa 'N') or n_a x m_a; x^p is n_a contiguous
+ * elements at X + p*ldxp, y^p m_a contiguous elements at Y + p*ldyp. */
+int kb_skron1(char transa, int64_t m_a, int64_t n_a, int64_t batch_count, float alpha, const float* A, int64_t lda,
+              int64_t lena, const float* X, int64_t ldxp, int64_t lenx, float beta, float* Y, int64_t ldyp,
+              int64_t leny, const kb_exec* exec, char* err, size_t errlen);
+int kb_dkron1(char transa, int64_t m_a, int64_t n_a, int64_t batch_count, double alpha, const double* A, int64_t lda,
+              int64_t lena, const double* X, int64_t ldxp, int64_t lenx, double beta, double* Y, int64_t ldyp,
+              int64_t leny, const kb_exec* exec, char* err, size_t errlen);
+
+/* C^p <- alpha * op(A^p) * op(B) + beta * C^p,  p < batch_count (gemm_a.hpp:9-17),
+ * replaces kronbatch::gemm_a<float|double> (proj/include/kronbatch/gemm_a.hpp:18-76).
+ * op(A^p) is m x k (A^p stored m x k or k x m with lda, at A + p*ldap), op(B)
+ * is k x n (B stored k x n or n x k with ldb), C^p is m x n with ldc at
+ * C + p*ldcp. parallel_hint is accepted and ignored (it only chunks the CPU
+ * worker loop in the reference). */
+int kb_sgemm_a(char transa, char transb, int64_t m, int64_t n, int64_t k, int64_t batch_count, float alpha,
+               const float* A, int64_t lda, int64_t ldap, int64_t lena, const float* B, int64_t ldb, int64_t lenb,
+               float beta, float* C, int64_t ldc, int64_t ldcp, int64_t lenc, const kb_exec* exec, char* err,
+               size_t errlen);
+int kb_dgemm_a(char transa, char transb, int64_t m, int64_t n, int64_t k, int64_t batch_count, double alpha,
+               const double* A, int64_t lda, int64_t ldap, int64_t lena, const double* B, int64_t ldb, int64_t lenb,
+               double beta, double* C, int64_t ldc, int64_t ldcp, int64_t lenc, const kb_exec* exec, char* err,
+               size_t errlen);
+
 /* Elements of workspace kron3 needs: m_a*m_b*n_c*batch_count. KB_EINVAL on
  * a negative dimension, KB_EOVERFLOW if the product overflows int64. */
 int kb_kron3_workspace_size(int64_t m_a, int64_t m_b, int64_t n_c, int64_t batch_count, int64_t* out, char* err,
@@ -114,7 +144,7 @@ const char* kb_version(void);
 /* kernels this process has launched through the library (all devices) */
 uint64_t kb_launch_count(void);
 /* name of the kernel the last call on this thread launched ("" if none):
- * "kron2_fast", "kron2_generic", "kron3_fast", "kron3_generic", "scale" */
+ * "kron2_fast", "kron2_generic", "kron3_fast", "kron3_generic", "kron1", "gemm_a", "scale" */
 const char* kb_last_path(void);
 /* release pooled device / pinned buffers held by the calling thread */
 void kb_release_buffers(void);

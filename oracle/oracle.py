@@ -59,6 +59,14 @@ class Oracle:
             f.restype = None
             f.argtypes = ([C.c_char] * 3 + [i64] * 7 + [T, vp, i64, vp, i64, vp, i64, vp, i64, i64, i64, T,
                                                        vp, i64, i64, i64])
+        for name, T in (("ko_skron1", C.c_float), ("ko_dkron1", C.c_double)):
+            f = getattr(L, name)
+            f.restype = None
+            f.argtypes = [C.c_char, i64, i64, i64, T, vp, i64, vp, i64, T, vp, i64]
+        for name, T in (("ko_sgemm_a", C.c_float), ("ko_dgemm_a", C.c_double)):
+            f = getattr(L, name)
+            f.restype = None
+            f.argtypes = [C.c_char, C.c_char, i64, i64, i64, i64, T, vp, i64, i64, vp, i64, T, vp, i64, i64]
         L.ko_generate_batch_f32.argtypes = [C.c_uint64, C.c_int, C.c_int, i64] + [vp] * 5
         L.ko_generate_batch_f64.argtypes = [C.c_uint64, C.c_int, C.c_int, i64] + [vp] * 5
         L.ko_set_fused.argtypes = [C.c_int]
@@ -110,6 +118,16 @@ class Oracle:
         f = self.lib.ko_skron3 if Y.dtype == np.float32 else self.lib.ko_dkron3
         f(_op(opa), _op(opb), _op(opc), m_a, n_a, m_b, n_b, m_c, n_c, batch, alpha, _ptr(A), lda, _ptr(B), ldb,
           _ptr(Cm), ldc, _ptr(X), ldx, ldx2, sx, beta, _ptr(Y), ldy, ldy2, sy)
+
+    def kron1(self, opa, m_a, n_a, batch, alpha, A, lda, X, sx, beta, Y, sy):
+        """kron1.hpp:17-62 restated (x entries contiguous n_a at p*sx, y m_a at p*sy)."""
+        f = self.lib.ko_skron1 if Y.dtype == np.float32 else self.lib.ko_dkron1
+        f(_op(opa), m_a, n_a, batch, alpha, _ptr(A), lda, _ptr(X), sx, beta, _ptr(Y), sy)
+
+    def gemm_a(self, opa, opb, m, n, k, batch, alpha, A, lda, sa, B, ldb, beta, Cm, ldc, sc):
+        """gemm_a.hpp:18-76 restated (A^p at p*sa, C^p at p*sc)."""
+        f = self.lib.ko_sgemm_a if Cm.dtype == np.float32 else self.lib.ko_dgemm_a
+        f(_op(opa), _op(opb), m, n, k, batch, alpha, _ptr(A), lda, sa, _ptr(B), ldb, beta, _ptr(Cm), ldc, sc)
 
     def kron3_workspace_size(self, m_a, m_b, n_c, batch):
         out = i64(0)
@@ -186,6 +204,16 @@ class Reference:
             f.argtypes = ([C.c_char] * 3 + [i64] * 7 + [T] + [vp, i64, i64, i64, i64] * 3 +
                           [vp, i64, i64, i64, i64, i64, i64, i64, T, vp, i64, i64, i64, i64, i64, i64, i64, vp, i64,
                            vp, C.c_size_t])
+        for name, T in (("kbref_skron1", C.c_float), ("kbref_dkron1", C.c_double)):
+            f = getattr(L, name)
+            f.restype = C.c_int
+            f.argtypes = [C.c_char, i64, i64, T, vp, i64, i64, i64, i64, vp, i64, i64, i64, i64, T, vp, i64, i64, i64,
+                          vp, C.c_size_t]
+        for name, T in (("kbref_sgemm_a", C.c_float), ("kbref_dgemm_a", C.c_double)):
+            f = getattr(L, name)
+            f.restype = C.c_int
+            f.argtypes = ([C.c_char, C.c_char, i64, i64, i64, T, vp, i64, i64, i64, i64, i64, i64, vp, i64, i64, i64,
+                           i64, T, vp, i64, i64, i64, i64, i64, i64, vp, C.c_size_t])
         L.kbref_generate_batch_f32.argtypes = [C.c_uint64, C.c_int, C.c_int, i64] + [vp] * 5
         L.kbref_generate_batch_f64.argtypes = [C.c_uint64, C.c_int, C.c_int, i64] + [vp] * 5
         L.kbref_has_openmp.restype = C.c_int
@@ -291,3 +319,24 @@ class Reference:
         K = np.empty((A.shape[0] * B.shape[0], A.shape[1] * B.shape[1]), np.float64, order="F")
         self.lib.kbref_kron_matrix(A.shape[0], A.shape[1], _ptr(A), B.shape[0], B.shape[1], _ptr(B), _ptr(K))
         return K
+
+    def kron1(self, opa, m_a, n_a, alpha, A, a_shape, lda, X, x_size, sx, batch, beta, Y, y_size, sy, lens=None):
+        """kronbatch::kron1<T> over views of the given arrays (proj/include/kronbatch/kron1.hpp:17-62)."""
+        err = C.create_string_buffer(512)
+        la, lx, ly = lens if lens is not None else (A.size, X.size, Y.size)
+        f = self.lib.kbref_skron1 if Y.dtype == np.float32 else self.lib.kbref_dkron1
+        rc = f(_op(opa), m_a, n_a, alpha, _ptr(A), a_shape[0], a_shape[1], lda, la, _ptr(X), x_size, sx, lx, batch,
+               beta, _ptr(Y), y_size, sy, ly, err, 512)
+        if rc:
+            self._raise(rc, err)
+
+    def gemm_a(self, opa, opb, m, n, k, alpha, A, a_shape, lda, sa, batch, B, b_shape, ldb, beta, Cm, c_shape, ldc, sc,
+               hint=0, lens=None):
+        """kronbatch::gemm_a<T> over views of the given arrays (proj/include/kronbatch/gemm_a.hpp:18-76)."""
+        err = C.create_string_buffer(512)
+        la, lb, lc = lens if lens is not None else (A.size, B.size, Cm.size)
+        f = self.lib.kbref_sgemm_a if Cm.dtype == np.float32 else self.lib.kbref_dgemm_a
+        rc = f(_op(opa), _op(opb), m, n, k, alpha, _ptr(A), a_shape[0], a_shape[1], lda, sa, la, batch, _ptr(B),
+               b_shape[0], b_shape[1], ldb, lb, beta, _ptr(Cm), c_shape[0], c_shape[1], ldc, sc, lc, hint, err, 512)
+        if rc:
+            self._raise(rc, err)

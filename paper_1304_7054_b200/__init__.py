@@ -3,7 +3,9 @@
 B200-native implementation of the hot path of arXiv:1304.7054 / the reference
 ``kronbatch`` library: ``kron2`` (Y = alpha op(A) op(X) op(B)^T + beta Y) and
 ``kron3`` (vec Y = alpha (C (x) B (x) A) vec X + beta vec Y) over large batches,
-fp32 / fp64, behind the reference's own API. See DESIGN.md.
+fp32 / fp64, behind the reference's own API -- plus the umbrella API's other two
+batched operators, ``kron1`` (shared-A GEMV) and ``gemm_a`` (varying-A GEMM).
+See DESIGN.md.
 """
 from ._lib import ABI_SYMBOLS, LIB_PATH, lib  # noqa: F401  (raises if the .so is missing)
 from .api import (  # noqa: F401
@@ -14,9 +16,12 @@ from .api import (  # noqa: F401
     KronProblem3D,
     MatrixOp,
     MatrixView,
+    VectorView,
     Workspace,
     footprint,
+    gemm_a,
     is_transposed,
+    kron1,
     kron2,
     kron3,
     kron3_workspace_size,
@@ -30,7 +35,7 @@ from .api import (  # noqa: F401
 )
 
 __all__ = [
-    "Array3View", "BatchView", "Exec", "KronProblem2D", "KronProblem3D", "MatrixOp", "MatrixView", "Workspace",
-    "footprint", "is_transposed", "kron2", "kron3", "kron3_workspace_size", "last_path", "launch_count", "op_dims",
+    "Array3View", "BatchView", "Exec", "KronProblem2D", "KronProblem3D", "MatrixOp", "MatrixView", "VectorView",
+    "Workspace", "footprint", "gemm_a", "is_transposed", "kron1", "kron2", "kron3", "kron3_workspace_size", "last_path", "launch_count", "op_dims",
     "release_buffers", "validate", "validate_batch", "version",
 ]

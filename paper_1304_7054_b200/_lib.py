@@ -23,6 +23,10 @@ ABI_SYMBOLS = (
     "kb_skron3",
     "kb_dkron3",
     "kb_kron3_workspace_size",
+    "kb_skron1",
+    "kb_dkron1",
+    "kb_sgemm_a",
+    "kb_dgemm_a",
     "kb_version",
     "kb_launch_count",
     "kb_last_path",
@@ -61,6 +65,16 @@ def _load(path: str = LIB_PATH):
         f.argtypes = [ch, ch, ch, i64, i64, i64, i64, i64, i64, i64, T, vp, i64, i64, vp, i64, i64, vp, i64, i64, vp,
                       i64, i64, i64, i64, T, vp, i64, i64, i64, i64, vp, i64, C.POINTER(KbExec), C.c_char_p,
                       C.c_size_t]
+    for name, T in (("kb_skron1", C.c_float), ("kb_dkron1", C.c_double)):
+        f = getattr(lib, name)
+        f.restype = C.c_int
+        f.argtypes = [ch, i64, i64, i64, T, vp, i64, i64, vp, i64, i64, T, vp, i64, i64, C.POINTER(KbExec),
+                      C.c_char_p, C.c_size_t]
+    for name, T in (("kb_sgemm_a", C.c_float), ("kb_dgemm_a", C.c_double)):
+        f = getattr(lib, name)
+        f.restype = C.c_int
+        f.argtypes = [ch, ch, i64, i64, i64, i64, T, vp, i64, i64, i64, vp, i64, i64, T, vp, i64, i64, i64,
+                      C.POINTER(KbExec), C.c_char_p, C.c_size_t]
     lib.kb_kron3_workspace_size.restype = C.c_int
     lib.kb_kron3_workspace_size.argtypes = [i64, i64, i64, i64, C.POINTER(i64), C.c_char_p, C.c_size_t]
     lib.kb_version.restype = C.c_char_p

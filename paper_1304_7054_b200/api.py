@@ -21,6 +21,8 @@ this module                 reference
                             ``OverflowError``)
 ``kron2``                   kron2.hpp:37-110
 ``kron3``                   kron3.hpp:72-166
+``kron1``, ``VectorView``   kron1.hpp:17-62, views.hpp:22-46
+``gemm_a``                  gemm_a.hpp:18-76
 ==========================  ==================================================
 
 Buffers are 1-D ``torch.Tensor`` (CUDA or CPU, pinned or pageable) or numpy
@@ -104,6 +106,23 @@ def _buf_info(data):
 
 
 @dataclass
+class VectorView:
+    """Contiguous vector of ``size`` elements (a kron1 batch entry; views.hpp:22-46)."""
+
+    data: Any
+    size: int
+    len: Optional[int] = None
+    offset: int = 0
+
+    def __post_init__(self):
+        if self.len is None:
+            self.len = _buf_info(self.data)[1] - self.offset
+
+    def shifted(self, off: int) -> "VectorView":
+        return VectorView(self.data, self.size, self.len - off, self.offset + off)
+
+
+@dataclass
 class MatrixView:
     """Column-major matrix: element (i, j) at flat index i + j*ld (views.hpp:51-83)."""
 
@@ -158,6 +177,8 @@ class BatchView:
 
 def footprint(v) -> int:
     """Elements an entry occupies (views.hpp:137-148)."""
+    if isinstance(v, VectorView):
+        return v.size
     if isinstance(v, MatrixView):
         return 0 if v.cols == 0 else v.ld * v.cols
     if isinstance(v, Array3View):
@@ -174,8 +195,13 @@ def _layout_error(context: str, what: str):
 
 
 def validate(v, context: str = "") -> None:
-    """views.hpp:198-223: raises ValueError describing the first violated invariant."""
-    if isinstance(v, MatrixView):
+    """views.hpp:190-223: raises ValueError describing the first violated invariant."""
+    if isinstance(v, VectorView):
+        if v.size < 0:
+            _layout_error(context, "size " + _nums(v.size, 0))
+        if v.len < v.size:
+            _layout_error(context, "buffer length " + _nums(v.len, v.size))
+    elif isinstance(v, MatrixView):
         if v.rows < 0 or v.cols < 0:
             _layout_error(context, "negative rows/cols")
         if v.ld < max(v.rows, 1):
@@ -409,6 +435,50 @@ def kron3(pr: KronProblem3D, a: MatrixView, b: MatrixView, c: MatrixView, x: Bat
           pb or None, b.ld, b.len, pc or None, c.ld, c.len, px or None, x.base.ld, x.base.ld2, x.batch_stride,
           x.base.len, pr.beta, py or None, y.base.ld, y.base.ld2, y.batch_stride, y.base.len, wp or None,
           work.capacity, exec_=exec_)
+
+
+def kron1(op_a, m_a: int, n_a: int, alpha, a: MatrixView, x: BatchView, beta, y: BatchView,
+          exec_: Optional[Exec] = None) -> None:
+    """y^p <- alpha * op(A) * x^p + beta * y^p (kron1.hpp:9-62): a batched GEMV
+    with A shared across the batch; x, y are batches of VectorView."""
+    validate(a, "kron1: A")
+    validate_batch(x, "kron1: X")
+    validate_batch(y, "kron1: Y")
+    ra, ca = op_dims(op_a, a.rows, a.cols)
+    if not (ra == m_a and ca == n_a):
+        _layout_error("kron1: A", f"op(A) is {_dim2s(ra, ca)}, expected {_dim2s(m_a, n_a)}")
+    _require(x.batch_count == y.batch_count, "kron1", "X and Y batch_count differ")
+    if x.base.size != n_a:
+        _layout_error("kron1: X", f"entry length {x.base.size}, expected {n_a}")
+    if y.base.size != m_a:
+        _layout_error("kron1: Y", f"entry length {y.base.size}, expected {m_a}")
+    (pa, px, py), dt = _ptrs_and_dtype(a, x.base, y.base)
+    fn = _lib.lib.kb_skron1 if dt == "float32" else _lib.lib.kb_dkron1
+    _call(fn, _opc(op_a), m_a, n_a, x.batch_count, alpha, pa or None, a.ld, a.len, px or None, x.batch_stride,
+          x.base.len, beta, py or None, y.batch_stride, y.base.len, exec_=exec_)
+
+
+def gemm_a(op_a, op_b, m: int, n: int, k: int, alpha, a: BatchView, b: MatrixView, beta, c: BatchView,
+           parallel_hint: int = 0, exec_: Optional[Exec] = None) -> None:
+    """C^p <- alpha * op(A^p) * op(B) + beta * C^p (gemm_a.hpp:9-76): a batched
+    GEMM with the left matrix varying and B shared. ``parallel_hint`` (a CPU
+    worker-chunk hint in the reference) does not change results and is ignored."""
+    validate_batch(a, "gemm_a: A")
+    validate(b, "gemm_a: B")
+    validate_batch(c, "gemm_a: C")
+    ram, rak = op_dims(op_a, a.base.rows, a.base.cols)
+    rbk, rbn = op_dims(op_b, b.rows, b.cols)
+    _require(a.batch_count == c.batch_count, "gemm_a", "A and C batch_count differ")
+    if not (ram == m and rak == k):
+        _layout_error("gemm_a: A", f"op(A) is {_dim2s(ram, rak)}, expected {_dim2s(m, k)}")
+    if not (rbk == k and rbn == n):
+        _layout_error("gemm_a: B", f"op(B) is {_dim2s(rbk, rbn)}, expected {_dim2s(k, n)}")
+    if not (c.base.rows == m and c.base.cols == n):
+        _layout_error("gemm_a: C", f"entry is {_dim2s(c.base.rows, c.base.cols)}, expected {_dim2s(m, n)}")
+    (pa, pb, pc), dt = _ptrs_and_dtype(a.base, b, c.base)
+    fn = _lib.lib.kb_sgemm_a if dt == "float32" else _lib.lib.kb_dgemm_a
+    _call(fn, _opc(op_a), _opc(op_b), m, n, k, a.batch_count, alpha, pa or None, a.base.ld, a.batch_stride,
+          a.base.len, pb or None, b.ld, b.len, beta, pc or None, c.base.ld, c.batch_stride, c.base.len, exec_=exec_)
 
 
 def launch_count() -> int:

@@ -1,0 +1,103 @@
+// kb_blas.cu -- the two other batched operators of the reference's umbrella
+// API (README.md:19-24), on the same launcher as kron2/kron3:
+//
+//   kron1  (proj/include/kronbatch/kron1.hpp:17-62): y^p <- alpha op(A) x^p + beta y^p,
+//          shared A, a batched GEMV. Reference arithmetic: gemm_axpy with
+//          R = x^p (detail.hpp:38-117): per element init from beta, then
+//          acc = fma(A_r(i, kk), fl(alpha x[kk]), acc), kk ascending.
+//   gemm_a (proj/include/kronbatch/gemm_a.hpp:18-76): C^p <- alpha op(A^p) op(B) + beta C^p,
+//          varying A, shared B. op_a = N: gemm_axpy with S = A^p, R = B_r
+//          (w = fl(alpha B_r(kk, c))); op_a = T: gemm_dot (detail.hpp:119-135):
+//          acc = sum_kk A^p(kk, i) B_r(kk, c) from 0, then
+//          fma(alpha, acc, beta == 0 ? 0 : fl(beta C)).
+//
+// Both are HBM-bound streaming operators (AI ~ n/4 .. n/2 flop/B): one thread
+// per output element, consecutive threads on consecutive rows of one entry so
+// the per-entry operand reads broadcast through L1 and the output writes are
+// coalesced; the shared matrix is read through the read-only path (it stays
+// in L1/L2). Any shape, op and stride; identical arithmetic to the CPU path.
+#include "kb_kernels.h"
+
+namespace kb {
+
+template <typename T>
+__global__ void kron1_kernel(const T* __restrict__ A, long long lda, int opa, const T* __restrict__ X,
+                             long long sx, T* __restrict__ Y, long long sy, long long m, long long n,
+                             long long batch, T alpha, int beta_mode, T beta) {
+  const long long total = batch * m;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long p = t / m, i = t - p * m;
+    const T* x = X + p * sx;
+    T* y = Y + p * sy + i;
+    T acc = beta_mode == kBetaZero ? T(0) : beta_init(beta_mode, beta, *y);
+    for (long long kk = 0; kk < n; ++kk) {
+      const T w = mul_rn(alpha, __ldg(x + kk));
+      acc = fma_rn(__ldg(opa ? A + kk + i * lda : A + i + kk * lda), w, acc);
+    }
+    *y = acc;
+  }
+}
+
+template <typename T>
+__global__ void gemm_a_kernel(const T* __restrict__ A, long long lda, long long sa, int opa,
+                              const T* __restrict__ B, long long ldb, int opb, T* __restrict__ Cm, long long ldc,
+                              long long sc, long long m, long long n, long long k, long long batch, T alpha,
+                              int beta_mode, T beta) {
+  const long long per = m * n, total = batch * per;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long p = t / per, r = t - p * per, c = r / m, i = r - c * m;
+    const T* a = A + p * sa;
+    T* out = Cm + p * sc + i + c * ldc;
+    auto b_at = [&](long long kk) { return __ldg(opb ? B + c + kk * ldb : B + kk + c * ldb); };  // B_r(kk, c)
+    if (!opa) {  // gemm_axpy: init, then + A(i, kk) * fl(alpha B_r(kk, c))
+      T acc = beta_mode == kBetaZero ? T(0) : beta_init(beta_mode, beta, *out);
+      for (long long kk = 0; kk < k; ++kk) acc = fma_rn(__ldg(a + i + kk * lda), mul_rn(alpha, b_at(kk)), acc);
+      *out = acc;
+    } else {  // gemm_dot: plain dot from 0, then alpha * acc + beta * C
+      T acc = T(0);
+      for (long long kk = 0; kk < k; ++kk) acc = fma_rn(__ldg(a + kk + i * lda), b_at(kk), acc);
+      const T init = beta_mode == kBetaZero ? T(0) : mul_rn(beta, *out);
+      *out = fma_rn(alpha, acc, init);
+    }
+  }
+}
+
+template <typename T>
+cudaError_t launch_kron1(const T* A, long long lda, int opa, const T* X, long long sx, T* Y, long long sy,
+                         long long m, long long n, long long batch, T alpha, int beta_mode, T beta, int sm_count,
+                         cudaStream_t s) {
+  const long long total = batch * m;
+  const int threads = 256;
+  const long long want = (total + threads - 1) / threads;
+  const int grid = (int)(want < (long long)sm_count * 16 ? want : (long long)sm_count * 16);
+  kron1_kernel<T><<<grid, threads, 0, s>>>(A, lda, opa, X, sx, Y, sy, m, n, batch, alpha, beta_mode, beta);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_gemm_a(const T* A, long long lda, long long sa, int opa, const T* B, long long ldb, int opb, T* Cm,
+                          long long ldc, long long sc, long long m, long long n, long long k, long long batch, T alpha,
+                          int beta_mode, T beta, int sm_count, cudaStream_t s) {
+  const long long total = batch * m * n;
+  const int threads = 256;
+  const long long want = (total + threads - 1) / threads;
+  const int grid = (int)(want < (long long)sm_count * 16 ? want : (long long)sm_count * 16);
+  gemm_a_kernel<T><<<grid, threads, 0, s>>>(A, lda, sa, opa, B, ldb, opb, Cm, ldc, sc, m, n, k, batch, alpha,
+                                            beta_mode, beta);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_kron1<float>(const float*, long long, int, const float*, long long, float*, long long,
+                                         long long, long long, long long, float, int, float, int, cudaStream_t);
+template cudaError_t launch_kron1<double>(const double*, long long, int, const double*, long long, double*, long long,
+                                          long long, long long, long long, double, int, double, int, cudaStream_t);
+template cudaError_t launch_gemm_a<float>(const float*, long long, long long, int, const float*, long long, int,
+                                          float*, long long, long long, long long, long long, long long, long long,
+                                          float, int, float, int, cudaStream_t);
+template cudaError_t launch_gemm_a<double>(const double*, long long, long long, int, const double*, long long, int,
+                                           double*, long long, long long, long long, long long, long long, long long,
+                                           double, int, double, int, cudaStream_t);
+
+}  // namespace kb

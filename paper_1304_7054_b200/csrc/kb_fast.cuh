@@ -376,10 +376,10 @@ struct Kron2Fast {
   }
 };
 
-template <typename T, int N, int OPX, int V>
+template <typename T, int N, int OPX, int V, bool YS>
 __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
-    kron2_sq_kernel(const Kron2Params<T> p, const __grid_constant__ SqConsts2<T, N> kc, const long long ngroups,
-                    const int ystage) {
+    kron2_sq_kernel(const Kron2Params<T> p, const __grid_constant__ SqConsts2<T, N> kc, const long long ngroups) {
+  constexpr bool ystage = YS;  // Y staged through the entry's smem slot (compile-time: no dead code in the other)
   using K = Kron2Fast<T, N, V>;
   using C = SqCfg<T, N>;
   constexpr int R = C::R, TPI = C::TPI, IPW = C::IPW, NN = C::NN, VXC = C::VXC, S = K::STAGES;
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
     T* sbase = wring + stage * K::RING;  // entry 0 of the group (span copies land shifted)
     if (!K::BULK && span) sbase += (reinterpret_cast<uintptr_t>(p.X + g * IPW * NN) & 15) / sizeof(T);
     T* xs = sbase + slot * C::SLOT;
-    if (ystage) {
+    if constexpr (ystage) {
       // Y(I_q, j) goes into the entry's own smem slot (X is dead once every
       // lane of the entry finished mode 1), then leaves with coalesced stores.
       T t[N][R];
@@ -581,10 +581,10 @@ struct Kron3Fast {
   }
 };
 
-template <typename T, int N, int V>
+template <typename T, int N, int V, bool YS>
 __global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS, Kron3Fast<T, N, V>::MINB)
-    kron3_sq_kernel(const Kron3Params<T> p, const __grid_constant__ SqConsts3<T, N> kc, const long long ntiles,
-                    const int ystage) {
+    kron3_sq_kernel(const Kron3Params<T> p, const __grid_constant__ SqConsts3<T, N> kc, const long long ntiles) {
+  constexpr bool ystage = YS;
   using K = Kron3Fast<T, N, V>;
   using C = SqCfg<T, N>;
   constexpr int R = C::R, TPI = C::TPI, NN = C::NN, VXC = C::VXC, IT = K::IT, PS = K::PS, S = K::STAGES;
@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS, Kron3Fast<T, N, V
           for (int kk = 0; kk < K::KB; ++kk)
             if (k0 + kk < N) init_y<T, N>(y[kk], yb + (long long)(k0 + kk) * p.ldy2, rows, p.beta_mode, p.beta);
           contract_rows_c<T, N, K::KB>(y, f, kc.c, k0);
-          if (ystage) {
+          if constexpr (ystage) {
             // Y(I_q, fj, k) overwrites T2(I_q, fj, n = k): exactly the fiber
             // this thread read above, so no other thread is affected.
             T* fw = buf + fe * K::ITEM + fj * N + q * R;
@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(Kron3Fast<T, N, V>::THREADS, Kron3Fast<T, N, V
         }
       }
     }
-    if (ystage) {
+    if constexpr (ystage) {
       __syncthreads();
       const long long first = tile * IT;
       const int valid = (int)(p.batch - first < IT ? p.batch - first : IT);

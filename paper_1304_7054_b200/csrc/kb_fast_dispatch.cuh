@@ -74,7 +74,8 @@ static cudaError_t launch2v(const Kron2Params<T>& p, const T* ha, const T* hw, i
   if (p.ldx != N || p.sx % C::VXC || !aligned<T>(p.X, C::VXC)) return cudaErrorNotSupported;
   if (K::BULK && ((p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))) return cudaErrorNotSupported;
   if (p.ldy % C::VY || p.sy % C::VY || !aligned<T>(p.Y, C::VY)) return cudaErrorNotSupported;
-  auto kern = kron2_sq_kernel<T, N, OPX, V>;
+  const bool ys = want_ystage<T, N, 2>(p.ldy == N && p.sy % C::VXC == 0 && aligned<T>(p.Y, C::VXC));
+  auto kern = ys ? kron2_sq_kernel<T, N, OPX, V, true> : kron2_sq_kernel<T, N, OPX, V, false>;
   const int threads = K::WARPS * 32;
   const size_t smem = K::smem_bytes();
   const int occ = occupancy_for(kern, threads, smem);
@@ -87,8 +88,7 @@ static cudaError_t launch2v(const Kron2Params<T>& p, const T* ha, const T* hw, i
     kc.a[i] = ha[i];
     kc.w[i] = hw[i];
   }
-  const bool ys = want_ystage<T, N, 2>(p.ldy == N && p.sy % C::VXC == 0 && aligned<T>(p.Y, C::VXC));
-  kern<<<grid, threads, smem, s>>>(p, kc, ngroups, ys ? 1 : 0);
+  kern<<<grid, threads, smem, s>>>(p, kc, ngroups);
   return cudaGetLastError();
 }
 
@@ -171,7 +171,9 @@ static cudaError_t launch3v(const Kron3Params<T>& p, const T* ha, const T* hb, c
     return cudaErrorNotSupported;
   if (K::BULK && ((p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))) return cudaErrorNotSupported;
   if (p.ldy % C::VY || p.ldy2 % C::VY || p.sy % C::VY || !aligned<T>(p.Y, C::VY)) return cudaErrorNotSupported;
-  auto kern = kron3_sq_kernel<T, N, V>;
+  const bool ys = want_ystage<T, N, 3>(p.ldy == N && p.ldy2 == (long long)N * N && p.sy % C::VXC == 0 &&
+                                    aligned<T>(p.Y, C::VXC));
+  auto kern = ys ? kron3_sq_kernel<T, N, V, true> : kron3_sq_kernel<T, N, V, false>;
   const size_t smem = K::smem_bytes();
   const int occ = occupancy_for(kern, K::THREADS, smem);
   if (occ <= 0) return cudaErrorNotSupported;
@@ -183,9 +185,7 @@ static cudaError_t launch3v(const Kron3Params<T>& p, const T* ha, const T* hb, c
     kc.b[i] = hb[i];
     kc.c[i] = hc[i];
   }
-  const bool ys = want_ystage<T, N, 3>(p.ldy == N && p.ldy2 == (long long)N * N && p.sy % C::VXC == 0 &&
-                                    aligned<T>(p.Y, C::VXC));
-  kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles, ys ? 1 : 0);
+  kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
   return cudaGetLastError();
 }
 

@@ -34,6 +34,16 @@ template <typename T>
 cudaError_t launch_kron3_fast(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
                               cudaStream_t s);
 
+// kron1 / gemm_a (kb_blas.cu): any shape, op, stride; one thread per output.
+template <typename T>
+cudaError_t launch_kron1(const T* A, long long lda, int opa, const T* X, long long sx, T* Y, long long sy,
+                         long long m, long long n, long long batch, T alpha, int beta_mode, T beta, int sm_count,
+                         cudaStream_t s);
+template <typename T>
+cudaError_t launch_gemm_a(const T* A, long long lda, long long sa, int opa, const T* B, long long ldb, int opb, T* Cm,
+                          long long ldc, long long sc, long long m, long long n, long long k, long long batch, T alpha,
+                          int beta_mode, T beta, int sm_count, cudaStream_t s);
+
 // 3-D fp32 n = 16 on tcgen05 tensor cores with 3xTF32 compensation
 // (tolerance-level parity, not bit-exact). Same host constant layouts.
 cudaError_t launch_kron3_tc(const Kron3Params<float>& p, const float* ha, const float* hb, const float* hc,

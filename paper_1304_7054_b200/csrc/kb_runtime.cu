@@ -486,6 +486,136 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
   }
 }
 
+// ------------------------------------------------- kron1 / gemm_a --------
+// The other two operators of the reference API (kron1.hpp:17-62,
+// gemm_a.hpp:18-76) on the same staging / sharding launcher: per-entry
+// operand X (kron1 x^p, gemm_a A^p) streamed, shared matrix (kron1 A,
+// gemm_a B) uploaded once per slice, output Y (y^p, C^p).
+
+// validate(VectorView) views.hpp:190-195
+void validate_vector(const std::string& ctx, i64 size, i64 len) {
+  if (size < 0) layout_error(ctx, "size " + nums(size, 0));
+  if (len < size) layout_error(ctx, "buffer length " + nums(len, size));
+}
+
+template <typename T>
+int kron1_entry(char ta, i64 m_a, i64 n_a, i64 batch, T alpha, const T* A, i64 lda, i64 lena, const T* X, i64 ldxp,
+                i64 lenx, T beta, T* Y, i64 ldyp, i64 leny, const kb_exec* exec, char* err, size_t errlen) {
+  t_last_path.clear();
+  try {
+    check_op("kron1: A", ta);
+    const i64 ar = is_t(ta) ? n_a : m_a, ac = is_t(ta) ? m_a : n_a;
+    validate_matrix("kron1: A", ar, ac, lda, lena);  // kron1.hpp:24-26
+    validate_batch("kron1: X", batch, ldxp, n_a, lenx, [&] { validate_vector("kron1: X", n_a, lenx); });
+    validate_batch("kron1: Y", batch, ldyp, m_a, leny, [&] { validate_vector("kron1: Y", m_a, leny); });
+    if (batch == 0 || m_a == 0) return KB_OK;  // kron1.hpp:42
+    const bool scale_only = alpha == T(0) || n_a == 0;  // kron1.hpp:45
+    if (scale_only && beta == T(1)) return KB_OK;
+    const PtrInfo xi = classify(X), yi = classify(Y);
+    const bool x_dev = !scale_only && xi.device, y_dev = yi.device;
+    const int dev0 = y_dev ? yi.dev : (x_dev ? xi.dev : current_device());
+    StageSpec sp{ldxp, n_a, ldyp, m_a, beta != T(0) || ldyp != m_a, !scale_only, sizeof(T)};
+    cudaStream_t us = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
+    const bool sync = !(exec && (exec->flags & KB_EXEC_ASYNC) && (x_dev || scale_only) && y_dev);
+    const int bmode = beta_mode_of((double)beta);
+    auto slice = [&](int dev, i64 p0, i64 p1) {
+      const T* Ad = nullptr;
+      run_slice(
+          dev, X, Y, p0, p1, sp, x_dev && xi.dev == dev, y_dev && yi.dev == dev, us, sync,
+          [&](DevRes& r, cudaStream_t s) {
+            if (scale_only) return;  // A, X never read (kron1.hpp:45-55)
+            const i64 fa = fp_matrix(ac, lda);
+            T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + 32)));
+            Ad = const_on_device(A, fa, r.device, cs, s);
+          },
+          [&](const void* xd, void* yd, i64 n, DevRes& r, cudaStream_t s, int) {
+            if (scale_only) {
+              const int grid = (int)std::max<i64>(1, std::min<i64>((n * m_a + 255) / 256, (i64)r.sm_count * 16));
+              cuda_check(kb::launch_scale<T>(static_cast<T*>(yd), n, m_a, 1, 1, m_a, 0, ldyp, bmode, beta, grid, s),
+                         "kron1");
+              count_launch("scale");
+            } else {
+              cuda_check(kb::launch_kron1<T>(Ad, lda, is_t(ta), static_cast<const T*>(xd), ldxp, static_cast<T*>(yd),
+                                             ldyp, m_a, n_a, n, alpha, bmode, beta, r.sm_count, s),
+                         "kron1");
+              count_launch("kron1");
+            }
+          });
+    };
+    if (x_dev || y_dev)
+      slice(dev0, 0, batch);
+    else
+      shard(exec, dev0, batch, slice);
+    return KB_OK;
+  } catch (const Fail& f) {
+    return report(f, err, errlen);
+  } catch (const std::exception& e) {
+    return report(Fail{KB_EINTERNAL, std::string("kron1: ") + e.what()}, err, errlen);
+  }
+}
+
+template <typename T>
+int gemm_a_entry(char ta, char tb, i64 m, i64 n, i64 k, i64 batch, T alpha, const T* A, i64 lda, i64 ldap, i64 lena,
+                 const T* B, i64 ldb, i64 lenb, T beta, T* Cm, i64 ldc, i64 ldcp, i64 lenc, const kb_exec* exec,
+                 char* err, size_t errlen) {
+  t_last_path.clear();
+  try {
+    check_op("gemm_a: A", ta);
+    check_op("gemm_a: B", tb);
+    const i64 ar = is_t(ta) ? k : m, ac = is_t(ta) ? m : k;
+    const i64 br = is_t(tb) ? n : k, bc = is_t(tb) ? k : n;
+    const i64 fpa = fp_matrix(ac, lda), fpc = fp_matrix(n, ldc);
+    // gemm_a.hpp:24-26
+    validate_batch("gemm_a: A", batch, ldap, fpa, lena, [&] { validate_matrix("gemm_a: A", ar, ac, lda, lena); });
+    validate_matrix("gemm_a: B", br, bc, ldb, lenb);
+    validate_batch("gemm_a: C", batch, ldcp, fpc, lenc, [&] { validate_matrix("gemm_a: C", m, n, ldc, lenc); });
+    if (batch == 0 || m == 0 || n == 0) return KB_OK;  // gemm_a.hpp:44
+    const bool scale_only = alpha == T(0) || k == 0;   // gemm_a.hpp:46
+    if (scale_only && beta == T(1)) return KB_OK;
+    const PtrInfo ai = classify(A), ci = classify(Cm);
+    const bool a_dev = !scale_only && ai.device, c_dev = ci.device;
+    const int dev0 = c_dev ? ci.dev : (a_dev ? ai.dev : current_device());
+    StageSpec sp{ldap, fpa, ldcp, fpc, beta != T(0) || ldc != m || ldcp != m * n, !scale_only, sizeof(T)};
+    cudaStream_t us = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
+    const bool sync = !(exec && (exec->flags & KB_EXEC_ASYNC) && (a_dev || scale_only) && c_dev);
+    const int bmode = beta_mode_of((double)beta);
+    auto slice = [&](int dev, i64 p0, i64 p1) {
+      const T* Bd = nullptr;
+      run_slice(
+          dev, A, Cm, p0, p1, sp, a_dev && ai.dev == dev, c_dev && ci.dev == dev, us, sync,
+          [&](DevRes& r, cudaStream_t s) {
+            if (scale_only) return;  // A, B never read (gemm_a.hpp:46-58)
+            const i64 fb = fp_matrix(bc, ldb);
+            T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fb + 32)));
+            Bd = const_on_device(B, fb, r.device, cs, s);
+          },
+          [&](const void* ad, void* cd, i64 nb, DevRes& r, cudaStream_t s, int) {
+            if (scale_only) {
+              const int grid = (int)std::max<i64>(1, std::min<i64>((nb * m * n + 255) / 256, (i64)r.sm_count * 16));
+              cuda_check(kb::launch_scale<T>(static_cast<T*>(cd), nb, m, n, 1, ldc, 0, ldcp, bmode, beta, grid, s),
+                         "gemm_a");
+              count_launch("scale");
+            } else {
+              cuda_check(kb::launch_gemm_a<T>(static_cast<const T*>(ad), lda, ldap, is_t(ta), Bd, ldb, is_t(tb),
+                                              static_cast<T*>(cd), ldc, ldcp, m, n, k, nb, alpha, bmode, beta,
+                                              r.sm_count, s),
+                         "gemm_a");
+              count_launch("gemm_a");
+            }
+          });
+    };
+    if (a_dev || c_dev)
+      slice(dev0, 0, batch);
+    else
+      shard(exec, dev0, batch, slice);
+    return KB_OK;
+  } catch (const Fail& f) {
+    return report(f, err, errlen);
+  } catch (const std::exception& e) {
+    return report(Fail{KB_EINTERNAL, std::string("gemm_a: ") + e.what()}, err, errlen);
+  }
+}
+
 // --------------------------------------------------------- kron3 ---------
 
 template <typename T>
@@ -665,6 +795,33 @@ int kb_dkron3(char transa, char transb, char transc, int64_t m_a, int64_t n_a, i
   return kron3_entry<double>(transa, transb, transc, m_a, n_a, m_b, n_b, m_c, n_c, batch_count, alpha, A, lda,
                              lena, B, ldb, lenb, C, ldc, lenc, X, ldx, ldx2, ldxp, lenx, beta, Y, ldy, ldy2, ldyp,
                              leny, work, work_capacity, exec, err, errlen);
+}
+
+int kb_skron1(char transa, int64_t m_a, int64_t n_a, int64_t batch_count, float alpha, const float* A, int64_t lda,
+              int64_t lena, const float* X, int64_t ldxp, int64_t lenx, float beta, float* Y, int64_t ldyp,
+              int64_t leny, const kb_exec* exec, char* err, size_t errlen) {
+  return kron1_entry<float>(transa, m_a, n_a, batch_count, alpha, A, lda, lena, X, ldxp, lenx, beta, Y, ldyp, leny,
+                            exec, err, errlen);
+}
+int kb_dkron1(char transa, int64_t m_a, int64_t n_a, int64_t batch_count, double alpha, const double* A, int64_t lda,
+              int64_t lena, const double* X, int64_t ldxp, int64_t lenx, double beta, double* Y, int64_t ldyp,
+              int64_t leny, const kb_exec* exec, char* err, size_t errlen) {
+  return kron1_entry<double>(transa, m_a, n_a, batch_count, alpha, A, lda, lena, X, ldxp, lenx, beta, Y, ldyp, leny,
+                             exec, err, errlen);
+}
+int kb_sgemm_a(char transa, char transb, int64_t m, int64_t n, int64_t k, int64_t batch_count, float alpha,
+               const float* A, int64_t lda, int64_t ldap, int64_t lena, const float* B, int64_t ldb, int64_t lenb,
+               float beta, float* C, int64_t ldc, int64_t ldcp, int64_t lenc, const kb_exec* exec, char* err,
+               size_t errlen) {
+  return gemm_a_entry<float>(transa, transb, m, n, k, batch_count, alpha, A, lda, ldap, lena, B, ldb, lenb, beta, C,
+                             ldc, ldcp, lenc, exec, err, errlen);
+}
+int kb_dgemm_a(char transa, char transb, int64_t m, int64_t n, int64_t k, int64_t batch_count, double alpha,
+               const double* A, int64_t lda, int64_t ldap, int64_t lena, const double* B, int64_t ldb, int64_t lenb,
+               double beta, double* C, int64_t ldc, int64_t ldcp, int64_t lenc, const kb_exec* exec, char* err,
+               size_t errlen) {
+  return gemm_a_entry<double>(transa, transb, m, n, k, batch_count, alpha, A, lda, ldap, lena, B, ldb, lenb, beta, C,
+                              ldc, ldcp, lenc, exec, err, errlen);
 }
 
 int kb_kron3_workspace_size(int64_t m_a, int64_t m_b, int64_t n_c, int64_t batch_count, int64_t* out, char* err,

@@ -13,6 +13,7 @@ import csv
 import glob
 import json
 import os
+import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -20,7 +21,8 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 from ncu_summary import summarise  # noqa: E402
 
 WORKLOAD_OF = {"prof_kron2_f32_n16": "kron2-f32-n16", "prof_kron3_f32_n16": "kron3-f32-n16",
-               "prof_kron3_f64_n16": "kron3-f64-n16", "prof_kron3tc_f32_n16": "kron3-f32-n16-tf32"}
+               "prof_kron3_f64_n16": "kron3-f64-n16", "prof_kron3tc_f32_n16": "kron3-f32-n16-tf32",
+               "prof_kron3_f32_n10": "kron3-f32-n10", "prof_kron2_f32_n10": "kron2-f32-n10"}
 
 
 def num(v):
@@ -69,6 +71,10 @@ def main(tag):
         summ = summarise(rep)
         with open(os.path.join(out_dir, f"{tag}_{base}.json"), "w") as f:
             json.dump({"report": base, "launches": summ}, f, indent=1)
+        src = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_source.py"), rep, "20"],
+                             capture_output=True, text=True).stdout
+        with open(os.path.join(out_dir, f"{tag}_{base}_stalls.txt"), "w") as f:
+            f.write(src)
         wl = WORKLOAD_OF.get(base)
         if wl and summ:
             s = summ[0]
