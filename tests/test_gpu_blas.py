@@ -124,7 +124,7 @@ def test_gemm_a_padding_nan_alpha0_zero_dims_host():
     got2 = run_gemm_a("N", "N", m, n, k, 0.0, np.full(m * k * batch, np.nan), m, m * k, batch, np.full(k * n, np.nan), k,
                       -1.0, C2, m, m * n)
     assert np.array_equal(got2, -C2)
-    got3 = run_gemm_a("N", "N", m, n, 0, 2.0, np.zeros(0), m, 0, batch, np.zeros(0), 1, 0.5, C2, m, m * n)
+    got3 = run_gemm_a("N", "N", m, n, 0, 2.0, np.zeros(1), m, 0, batch, np.full(n, np.nan), 1, 0.5, C2, m, m * n)
     assert np.array_equal(got3, 0.5 * C2)  # k = 0: empty sum
     # host-staged buffers: same bits as device-resident
     A4, B4, C4 = uniform(g, k * m * batch, np.float32), uniform(g, k * n, np.float32), uniform(g, m * n * batch, np.float32)
