@@ -23,6 +23,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libkronref.so")
+REF_BLAS_SO = os.path.join(HERE, "_ref", "libkronref_blas.so")
 
 i64 = C.c_int64
 vp = C.c_void_p
@@ -204,13 +205,15 @@ class Reference:
             f.argtypes = ([C.c_char] * 3 + [i64] * 7 + [T] + [vp, i64, i64, i64, i64] * 3 +
                           [vp, i64, i64, i64, i64, i64, i64, i64, T, vp, i64, i64, i64, i64, i64, i64, i64, vp, i64,
                            vp, C.c_size_t])
-        for name, T in (("kbref_skron1", C.c_float), ("kbref_dkron1", C.c_double)):
-            f = getattr(L, name)
+        # kron1 / gemm_a live in their own library (ref_shim_blas.cpp explains why)
+        BL = self.blas = C.CDLL(REF_BLAS_SO) if os.path.exists(REF_BLAS_SO) else None
+        for name, T in ((("kbref_skron1", C.c_float), ("kbref_dkron1", C.c_double)) if BL else ()):
+            f = getattr(BL, name)
             f.restype = C.c_int
             f.argtypes = [C.c_char, i64, i64, T, vp, i64, i64, i64, i64, vp, i64, i64, i64, i64, T, vp, i64, i64, i64,
                           vp, C.c_size_t]
-        for name, T in (("kbref_sgemm_a", C.c_float), ("kbref_dgemm_a", C.c_double)):
-            f = getattr(L, name)
+        for name, T in ((("kbref_sgemm_a", C.c_float), ("kbref_dgemm_a", C.c_double)) if BL else ()):
+            f = getattr(BL, name)
             f.restype = C.c_int
             f.argtypes = ([C.c_char, C.c_char, i64, i64, i64, T, vp, i64, i64, i64, i64, i64, i64, vp, i64, i64, i64,
                            i64, T, vp, i64, i64, i64, i64, i64, i64, vp, C.c_size_t])
@@ -324,7 +327,7 @@ class Reference:
         """kronbatch::kron1<T> over views of the given arrays (proj/include/kronbatch/kron1.hpp:17-62)."""
         err = C.create_string_buffer(512)
         la, lx, ly = lens if lens is not None else (A.size, X.size, Y.size)
-        f = self.lib.kbref_skron1 if Y.dtype == np.float32 else self.lib.kbref_dkron1
+        f = self.blas.kbref_skron1 if Y.dtype == np.float32 else self.blas.kbref_dkron1
         rc = f(_op(opa), m_a, n_a, alpha, _ptr(A), a_shape[0], a_shape[1], lda, la, _ptr(X), x_size, sx, lx, batch,
                beta, _ptr(Y), y_size, sy, ly, err, 512)
         if rc:
@@ -335,7 +338,7 @@ class Reference:
         """kronbatch::gemm_a<T> over views of the given arrays (proj/include/kronbatch/gemm_a.hpp:18-76)."""
         err = C.create_string_buffer(512)
         la, lb, lc = lens if lens is not None else (A.size, B.size, Cm.size)
-        f = self.lib.kbref_sgemm_a if Cm.dtype == np.float32 else self.lib.kbref_dgemm_a
+        f = self.blas.kbref_sgemm_a if Cm.dtype == np.float32 else self.blas.kbref_dgemm_a
         rc = f(_op(opa), _op(opb), m, n, k, alpha, _ptr(A), a_shape[0], a_shape[1], lda, sa, la, batch, _ptr(B),
                b_shape[0], b_shape[1], ldb, lb, beta, _ptr(Cm), c_shape[0], c_shape[1], ldc, sc, lc, hint, err, 512)
         if rc:

@@ -84,10 +84,10 @@ struct Cw2 {
   static constexpr size_t smem_bytes() { return (size_t)ES * WARPS * STAGES * RING + 8 * WARPS * STAGES; }
 };
 
-template <typename T, int N>
+template <typename T, int N, bool YS>
 __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
-    kron2_cw_kernel(const Kron2Params<T> p, const __grid_constant__ SqConsts2<T, N> kc, const long long ngroups,
-                    const int ystage) {
+    kron2_cw_kernel(const Kron2Params<T> p, const __grid_constant__ SqConsts2<T, N> kc, const long long ngroups) {
+  constexpr bool ystage = YS;  // compile-time: the other store path is not even in the binary
   using K = Cw2<T, N>;
   constexpr int R = K::R, TPI = K::TPI, EPW = K::EPW, NN = K::NN, S = K::STAGES, SLOT = K::SLOT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
 #pragma unroll
         for (int j = 0; j < N; ++j) axpy_rows<R>(acc[j], t, kc.w[j * N + m]);
       }
-      if (ystage) {  // Y(I_q, j) over tmp(I_q, m = j): the rows this lane read
+      if constexpr (ystage) {  // Y(I_q, j) over tmp(I_q, m = j): the rows this lane read
 #pragma unroll
         for (int j = 0; j < N; ++j) {
           if constexpr (K::VR == 2 && sizeof(T) == 4)
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
       }
     }
     }
-    if (ystage) {
+    if constexpr (ystage) {
       __syncwarp();
       copy_out<T, NN, (K::BULK || K::TINY ? K::VXC : 1)>(p.Y + first * p.sy, p.sy, base, SLOT, 0, 1, valid, lane, 32);
     }

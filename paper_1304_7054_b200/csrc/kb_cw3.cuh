@@ -160,10 +160,12 @@ __device__ __forceinline__ void axpy_pairs_c(double* acc, const double* a, doubl
   for (int i = 0; i < n; ++i) acc[i] = __fma_rn(a[i], s, acc[i]);
 }
 
-template <typename T, int N, int V>
+template <typename T, int N, int V, bool B0>
 __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
     kron3_cw_kernel(const Kron3Params<T> p, const __grid_constant__ SqConstsCw3<T, N> kc, const long long ntiles) {
   using K = Cw3<T, N, V>;
+  // B0: beta == 0 known at compile time (Y never read; the beta paths are not in the binary)
+  const int beta_mode = B0 ? kBetaZero : p.beta_mode;
   constexpr int R = K::R, TPI = K::TPI, NN = K::NN, IT = K::IT, NP = K::NP, PS = K::PS, S = K::STAGES;
   constexpr int ITEM = K::ITEM;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
       T acc[N][R];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        if (p.beta_mode == kBetaZero) {
+        if (beta_mode == kBetaZero) {
           acc[k][0] = T(0);
           acc[k][1] = T(0);
         } else {
@@ -309,8 +311,8 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
             y0[0] = yb[(long long)k * p.ldy2];
             y0[1] = T(0);
           }
-          acc[k][0] = beta_init(p.beta_mode, p.beta, y0[0]);
-          acc[k][1] = beta_init(p.beta_mode, p.beta, y0[1]);
+          acc[k][0] = beta_init(beta_mode, p.beta, y0[0]);
+          acc[k][1] = beta_init(beta_mode, p.beta, y0[1]);
         }
       }
 #pragma unroll kCwUnroll

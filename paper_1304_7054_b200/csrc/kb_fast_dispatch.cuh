@@ -54,7 +54,7 @@ static int env_variant(const char* name, int dflt = 0) {
 // Stage Y through shared memory + coalesced copy-out instead of the direct
 // R-row stores. Measured per size on B200 (profiles/r01_sweep_ystage.txt, r01_sweep2_span.txt):
 // it pays for 2-D wherever the row-block stores are narrow or scattered
-// (fp32: all n but 1, 2, 4, 8, 16; fp64: n = 3..8, 12) and loses everywhere
+// (fp32: n = 3, 5-11, 15; fp64: n = 3-8, 10, 12) and loses everywhere
 // else, including every 3-D case (the extra CTA barrier costs more than the
 // store coalescing gains). KB_YSTAGE=0 / 1 forces it off / on for sweeps.
 template <typename T, int N, int DIMS>
@@ -63,8 +63,8 @@ static bool want_ystage(bool legal) {
   if (!legal) return false;
   if (force >= 0) return force != 0;
   if (DIMS == 3) return false;
-  if (sizeof(T) == 4) return !(N <= 2 || N == 4 || N == 8 || N == 16);
-  return (N >= 3 && N <= 8) || N == 12;
+  if (sizeof(T) == 4) return (N == 3 || (N >= 5 && N <= 11) || N == 15);
+  return (N >= 3 && N <= 8) || N == 10 || N == 12;
 }
 
 template <typename T, int N, int OPX, int V>
@@ -109,7 +109,7 @@ static cudaError_t launch2cw(const Kron2Params<T>& p, const T* ha, const T* hw, 
     if (p.ldy != N || p.sy % vc || !aligned<T>(p.Y, vc)) ys = false;
   }
   if (!ys && K::VRY == 2 && (p.ldy % 2 || p.sy % 2 || !aligned<T>(p.Y, 2))) return cudaErrorNotSupported;
-  auto kern = kron2_cw_kernel<T, N>;
+  auto kern = ys ? kron2_cw_kernel<T, N, true> : kron2_cw_kernel<T, N, false>;
   const int threads = K::WARPS * 32;
   const size_t smem = K::smem_bytes();
   const int occ = occupancy_for(kern, threads, smem);
@@ -122,7 +122,7 @@ static cudaError_t launch2cw(const Kron2Params<T>& p, const T* ha, const T* hw, 
     kc.a[i] = ha[i];
     kc.w[i] = hw[i];
   }
-  kern<<<grid, threads, smem, s>>>(p, kc, ngroups, ys ? 1 : 0);
+  kern<<<grid, threads, smem, s>>>(p, kc, ngroups);
   return cudaGetLastError();
 }
 
@@ -134,9 +134,9 @@ static int k2_family() {
   static const int force = env_variant("KB_K2", -1);
   if (force >= 0) return force;
   // fastest family per size, measured on B200 (profiles/r01_k2_families.txt)
-  if (sizeof(T) == 4) return (N <= 5 || (N >= 9 && N <= 13) || N == 15) ? 1 : 0;
-  if (N == 3 || N == 8) return 2;
-  return (N <= 2 || (N >= 9 && N <= 11) || N == 13 || N == 14) ? 1 : 0;
+  if (sizeof(T) == 4) return (N <= 4 || (N >= 9 && N <= 13) || N == 15) ? 1 : 0;
+  if (N == 3 || N == 10 || N == 11 || N == 13) return 2;
+  return (N <= 2 || N == 8 || N == 9) ? 1 : 0;
 }
 
 template <typename T, int N, int OPX>
@@ -199,7 +199,7 @@ static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, 
               : p.sx != (long long)N * N * N)  // odd n: contiguous entries, one span copy per tile
     return cudaErrorNotSupported;
   if (K::VRY == 2 && (p.ldy % 2 || p.ldy2 % 2 || p.sy % 2 || !aligned<T>(p.Y, 2))) return cudaErrorNotSupported;
-  auto kern = kron3_cw_kernel<T, N, V>;
+  auto kern = p.beta_mode == kBetaZero ? kron3_cw_kernel<T, N, V, true> : kron3_cw_kernel<T, N, V, false>;
   const size_t smem = K::smem_bytes();
   const int occ = occupancy_for(kern, K::THREADS, smem);
   if (occ <= 0) return cudaErrorNotSupported;
