@@ -75,6 +75,8 @@ static cudaError_t launch2v(const Kron2Params<T>& p, const T* ha, const T* hw, i
   if (K::BULK && ((p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))) return cudaErrorNotSupported;
   if (p.ldy % C::VY || p.sy % C::VY || !aligned<T>(p.Y, C::VY)) return cudaErrorNotSupported;
   const bool ys = want_ystage<T, N, 2>(p.ldy == N && p.sy % C::VXC == 0 && aligned<T>(p.Y, C::VXC));
+  // (a compile-time beta == 0 specialisation, as the 3-D column-wise kernel
+  //  has, made these kernels SLOWER: 2-D n = 16 fp64 5.9 -> 5.0 TB/s)
   auto kern = ys ? kron2_sq_kernel<T, N, OPX, V, true> : kron2_sq_kernel<T, N, OPX, V, false>;
   const int threads = K::WARPS * 32;
   const size_t smem = K::smem_bytes();

@@ -126,7 +126,26 @@ struct Buf {
   }
 };
 
-constexpr int kSlots = 3;  // staged pipeline depth (chunks in flight)
+constexpr int kSlots = 4;  // staged pipeline streams / buffer slots allocated per device
+
+// Staged pipeline shape: chunks in flight (<= kSlots) and MiB of X+Y per
+// chunk; KB_STAGE_SLOTS / KB_STAGE_MB override the defaults for sweeps.
+int stage_slots() {
+  static const int v = [] {
+    const char* e = std::getenv("KB_STAGE_SLOTS");
+    const int n = e ? std::atoi(e) : 3;
+    return n < 1 ? 1 : (n > kSlots ? kSlots : n);
+  }();
+  return v;
+}
+long long stage_bytes() {
+  static const long long v = [] {
+    const char* e = std::getenv("KB_STAGE_MB");
+    const long long mb = e ? std::atoll(e) : 64;
+    return (mb < 1 ? 1 : mb) << 20;
+  }();
+  return v;
+}
 
 struct DevRes {
   int device = -1;
@@ -342,14 +361,15 @@ void run_slice(int dev, const void* X, void* Y, i64 p0, i64 p1, const StageSpec&
   cuda_check(cudaStreamSynchronize(r.slot_stream[0]), "synchronize");
   // staged: chunk so one slot holds ~64 MiB of X+Y
   const i64 per_entry = (sp.x_used && !x_dev ? sp.sx : 0) + (!y_dev ? sp.sy : 0);
-  const i64 target = (64ll << 20) / (i64)sp.es;
+  const i64 target = stage_bytes() / (i64)sp.es;
+  const int nslots = stage_slots();
   i64 chunk = std::max<i64>(1, per_entry > 0 ? target / per_entry : (p1 - p0));
   chunk = std::min(chunk, p1 - p0);
   if (user_stream) cuda_check(cudaStreamSynchronize(user_stream), "synchronize");
   i64 c = 0;
   for (i64 q0 = p0; q0 < p1; q0 += chunk, ++c) {
     const i64 q1 = std::min(p1, q0 + chunk), n = q1 - q0;
-    const int slot = (int)(c % kSlots);
+    const int slot = (int)(c % nslots);
     cudaStream_t s = r.slot_stream[slot];
     const char* xd = nullptr;
     if (sp.x_used) {
