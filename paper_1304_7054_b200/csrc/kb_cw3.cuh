@@ -375,10 +375,11 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_cta(unsigned* addr, unsigne
   return old;
 }
 
-template <typename T, int S, bool EARLY>
+template <typename T, int S, bool EARLY, bool B0>
 __global__ void __launch_bounds__(128, Cwp3<T, S, EARLY>::MINB)
     kron3_cwp_kernel(const Kron3Params<T> p, const __grid_constant__ SqConstsCw3<T, 16> kc, const long long ntiles) {
   using K = Cwp3<T, S, EARLY>;
+  const int beta_mode = B0 ? kBetaZero : p.beta_mode;
   constexpr int N = 16, NN = 256, R = 2, PS = K::PS, ITEM = N * PS;
   constexpr int VXR = 16 / sizeof(T);  // column chunk (16 bytes)
   constexpr int VR = 2;                // row pair
@@ -484,13 +485,13 @@ __global__ void __launch_bounds__(128, Cwp3<T, S, EARLY>::MINB)
       T acc[N][R];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        if (p.beta_mode == kBetaZero) {
+        if (beta_mode == kBetaZero) {
           acc[k][0] = acc[k][1] = T(0);
         } else {
           T y0[R];
           ldg_n<R, VR>(y0, yb + (long long)k * p.ldy2);
-          acc[k][0] = beta_init(p.beta_mode, p.beta, y0[0]);
-          acc[k][1] = beta_init(p.beta_mode, p.beta, y0[1]);
+          acc[k][0] = beta_init(beta_mode, p.beta, y0[0]);
+          acc[k][1] = beta_init(beta_mode, p.beta, y0[1]);
         }
       }
       // hand the stage back: the last warp through issues its refill

@@ -227,7 +227,7 @@ static cudaError_t launch3cwp(const Kron3Params<T>& p, const T* ha, const T* hb,
   if (p.ldx != N || p.ldx2 != (long long)N * N || (p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))
     return cudaErrorNotSupported;
   if (p.ldy % 2 || p.ldy2 % 2 || p.sy % 2 || !aligned<T>(p.Y, 2)) return cudaErrorNotSupported;
-  auto kern = kron3_cwp_kernel<T, S, EARLY>;
+  auto kern = p.beta_mode == kBetaZero ? kron3_cwp_kernel<T, S, EARLY, true> : kron3_cwp_kernel<T, S, EARLY, false>;
   const size_t smem = K::smem_bytes();
   const int occ = occupancy_for(kern, K::THREADS, smem);
   if (occ <= 0) return cudaErrorNotSupported;

@@ -141,7 +141,7 @@ int stage_slots() {
 long long stage_bytes() {
   static const long long v = [] {
     const char* e = std::getenv("KB_STAGE_MB");
-    const long long mb = e ? std::atoll(e) : 64;
+    const long long mb = e ? std::atoll(e) : 128;
     return (mb < 1 ? 1 : mb) << 20;
   }();
   return v;
