@@ -10,6 +10,7 @@
 
 #include "kb_cw2.cuh"
 #include "kb_cw3.cuh"
+#include "kb_tiny3.cuh"
 #include "kb_fast.cuh"
 #include "kb_kernels.h"
 #include "kb_sizes.h"
@@ -269,11 +270,38 @@ static cudaError_t launch3cwpp(const Kron3Params<T>& p, const T* ha, const T* hb
   return cudaGetLastError();
 }
 
+// Tiny-entry 3-D kernel (kb_tiny3.cuh), n <= 4, tight entries.
+template <typename T, int N>
+static cudaError_t launch3tiny(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
+                               cudaStream_t s) {
+  using K = Tiny3<T, N>;
+  constexpr long long E = (long long)N * N * N;
+  if (p.ldx != N || p.ldx2 != (long long)N * N || p.sx != E) return cudaErrorNotSupported;
+  if (p.ldy != N || p.ldy2 != (long long)N * N || p.sy != E) return cudaErrorNotSupported;
+  auto kern = kron3_tiny_kernel<T, N>;
+  const int threads = K::WARPS * 32;
+  const size_t smem = K::smem_bytes();
+  const int occ = occupancy_for(kern, threads, smem);
+  if (occ <= 0) return cudaErrorNotSupported;
+  const long long ngroups = (p.batch + 31) / 32;
+  const long long want = (ngroups + K::WARPS - 1) / K::WARPS;
+  const int grid = (int)(want < (long long)sm_count * occ ? want : (long long)sm_count * occ);
+  SqConsts3<T, N> kc;
+  for (int i = 0; i < N * N; ++i) {
+    kc.a[i] = ha[i];
+    kc.b[i] = hb[i];
+    kc.c[i] = hc[i];
+  }
+  kern<<<grid, threads, smem, s>>>(p, kc, ngroups);
+  return cudaGetLastError();
+}
+
 // 3-D kernel family per size: 0 = row-owner (kron3_sq_kernel), 1 = column-wise,
 // 2 = column-wise single stage, 3 = column-wise 128-thread tiles (fp32; = 1 for
 // fp64), 4 / 5 = n = 16 warp-plane kernel with 2 / 1 stages, 6 = n = 16
 // software-pipelined warp-plane kernel (3 stages), 7 / 8 = warp-plane with the
-// early stage release (1 / 2 stages). KB_K3 overrides
+// early stage release (1 / 2 stages); n <= 4 tight entries first try the
+// tiny-entry kernel (9 forces it; any other KB_K3 skips it). KB_K3 overrides
 // the default for sweeps.
 template <typename T, int N>
 static int k3_family() {
@@ -298,6 +326,16 @@ static int k3_family() {
 template <typename T, int N>
 static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
                            cudaStream_t s) {
+  if constexpr (N <= 4) {
+    // measured (profiles/r01_k3_families.txt): the tiny-entry kernel wins at
+    // fp32 n = 2-4 (n = 2: 1.1 -> 5.6 TB/s) and fp64 n = 2, 3
+    static const int force = env_variant("KB_K3", -1);
+    constexpr bool tiny_default = N >= 2 && (sizeof(T) == 4 || N <= 3);
+    if ((force < 0 && tiny_default) || force == 9) {
+      const cudaError_t e = launch3tiny<T, N>(p, ha, hb, hc, sm_count, s);
+      if (e != cudaErrorNotSupported) return e;
+    }
+  }
   if constexpr (N >= 3) {
     const int fam = k3_family<T, N>();
 #ifdef KB_SWEEP_VARIANTS  // n = 16 warp-plane experiments (profiles/r01_k3_families.txt): `make VARIANTS=1`

@@ -289,9 +289,9 @@ struct K2 {
 };
 
 // Launch the compute for entries [0, n) of device-resident X/Y views.
-template <typename T>
+template <typename T, typename Upload>
 void run2_device(const K2<T>& k, const T* A, const T* B, const T* ha, const T* hw, const T* X, T* Y, i64 n,
-                 DevRes& r, cudaStream_t s, int slot) {
+                 DevRes& r, cudaStream_t s, int slot, Upload&& upload) {
   Kron2Params<T> p{};
   p.A = A; p.B = B; p.X = X; p.Y = Y;
   p.lda = k.lda; p.ldb = k.ldb; p.ldx = k.ldx; p.sx = k.sx; p.ldy = k.ldy; p.sy = k.sy;
@@ -307,6 +307,7 @@ void run2_device(const K2<T>& k, const T* A, const T* B, const T* ha, const T* h
   }
   if (e != cudaErrorNotSupported) cuda_check(e, "kron2");
   cudaGetLastError();
+  if (!p.A) upload(s, p.A, p.B);  // square call the fast path declined: device constants now
   const int grid = (int)std::min<i64>(n, (i64)r.sm_count * 8);
   const i64 per = k.m_a * k.n_b;
   T* scratch = nullptr;
@@ -473,15 +474,22 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
       const T* Ad = nullptr;
       const T* Bd = nullptr;
       std::vector<T> ha, hw;  // host-resolved constants for the square fast path
+      auto upload = [&](DevRes& r, cudaStream_t s) {
+        if (Ad) return;
+        const i64 fa = fp_matrix(ac, lda), fb = fp_matrix(bc, ldb);
+        T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + fb + 64)));
+        Ad = const_on_device(A, fa, r.device, cs, s);
+        Bd = const_on_device(B, fb, r.device, cs + fa + 32, s);
+      };
       run_slice(
           dev, X, Y, p0, p1, sp, x_dev && xi.dev == dev, y_dev && yi.dev == dev, us, sync,
           [&](DevRes& r, cudaStream_t s) {
             if (scale_only) return;  // A, B never read (kron2.hpp:67-79)
-            const i64 fa = fp_matrix(ac, lda), fb = fp_matrix(bc, ldb);
-            T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + fb + 64)));
-            Ad = const_on_device(A, fa, r.device, cs, s);
-            Bd = const_on_device(B, fb, r.device, cs + fa + 32, s);
+            // device copies of A/B only feed the generic kernel (the fast
+            // kernels take host-resolved constants as parameters)
+            if (!square_fast) upload(r, s);
             if (square_fast) {
+              const i64 fa = fp_matrix(ac, lda), fb = fp_matrix(bc, ldb);
               ha = resolve_sq(fetch_host(A, fa, s), lda, is_t(ta), (int)m_a, false, T(1), false);
               hw = resolve_sq(fetch_host(B, fb, s), ldb, is_t(tb), (int)m_a, true, alpha, true);
             }
@@ -491,7 +499,13 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
               scale2_device<T>(k, static_cast<T*>(yd), n, r, s);
             else
               run2_device<T>(k, Ad, Bd, square_fast ? ha.data() : nullptr, square_fast ? hw.data() : nullptr,
-                             static_cast<const T*>(xd), static_cast<T*>(yd), n, r, s, slot);
+                             static_cast<const T*>(xd), static_cast<T*>(yd), n, r, s, slot,
+                             [&](cudaStream_t us2, const T*& pa, const T*& pb) {
+                               upload(r, us2);
+                               cuda_check(cudaStreamSynchronize(us2), "constant upload");  // later chunks use other streams
+                               pa = Ad;
+                               pb = Bd;
+                             });
           });
     };
     if (x_dev || y_dev)
@@ -698,13 +712,25 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
     auto slice = [&](int dev, i64 p0, i64 p1) {
       const T *Ad = nullptr, *Bd = nullptr, *Cd = nullptr;
       std::vector<T> ha, hb, hc;  // host-resolved constants for the square fast path
+      DevRes* rp = nullptr;
+      cudaStream_t up_stream = nullptr;
+      auto upload = [&]() {  // A/B/C on the device (in place when already resident)
+        if (Ad) return;
+        DevRes& r = *rp;
+        T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + fb + fc + 96)));
+        Ad = const_on_device(A, fa, r.device, cs, up_stream);
+        Bd = const_on_device(B, fb, r.device, cs + fa + 32, up_stream);
+        Cd = const_on_device(Cm, fc, r.device, cs + fa + fb + 64, up_stream);
+      };
       run_slice(dev, X, Y, p0, p1, sp, x_dev && xi.dev == dev, y_dev && yi.dev == dev, us, sync,
                 [&](DevRes& r, cudaStream_t s) {
+                  rp = &r;
+                  up_stream = s;
                   if (scale_only) return;  // A, B, C never read (kron3.hpp:113-128)
-                  T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + fb + fc + 96)));
-                  Ad = const_on_device(A, fa, r.device, cs, s);
-                  Bd = const_on_device(B, fb, r.device, cs + fa + 32, s);
-                  Cd = const_on_device(Cm, fc, r.device, cs + fa + fb + 64, s);
+                  // device copies of A/B/C only feed the generic kernel: the
+                  // fast kernels take the host-resolved constants as kernel
+                  // parameters, so square calls skip the uploads (lazy below)
+                  if (!square_fast) upload();
                   if (square_fast) {
                     ha = resolve_sq(fetch_host(A, fa, s), lda, is_t(ta), (int)m_a, false, T(1), false);
                     hb = resolve_sq(fetch_host(B, fb, s), ldb, is_t(tb), (int)m_a, true, T(1), false);
@@ -749,6 +775,14 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                   }
                   if (e != cudaErrorNotSupported) cuda_check(e, "kron3");
                   cudaGetLastError();
+                  if (!Ad) {  // a square call the fast path declined (layout): constants now
+                    up_stream = s;
+                    upload();
+                    cuda_check(cudaStreamSynchronize(s), "constant upload");
+                    p.A = Ad;
+                    p.B = Bd;
+                    p.C = Cd;
+                  }
                   const int grid = (int)std::min<i64>(n, (i64)r.sm_count * 8);
                   const i64 per = m_a * n_b + m_a * m_b * n_c;
                   T* scratch = nullptr;
