@@ -62,21 +62,44 @@ __host__ __device__ constexpr int phase_banks(F off, int lanes, int words) {
 template <typename T, int N, int V = 0>
 struct Cw3 {
   static constexpr int ES = sizeof(T);
-  static constexpr int R = 2;                 // rows per mode-2/3 task (odd n: the last task has 1)
+  // rows per mode-2/3 task (odd n: the last task has 1). V3: one row per
+  // task -- twice the threads per entry (n = 16: 256), FFMA2 then pairs two
+  // output COLUMNS with a uniform-register constant pair, like mode 1
+  static constexpr int R = V == 3 ? 1 : 2;
   static constexpr int TPI = (N + 1) / R;     // tasks per plane / per fiber column
   static constexpr int NN = N * N;
   // entries per tile: ~256 threads of mode-2/3 tasks (fp32, V0/V1), ~128
   // (fp64; fp32 V2: 4-warp CTAs, so each SM sub-partition interleaves warps
   // of six independent CTAs instead of three)
   static constexpr int MAXT = ES == 4 && V != 2 ? 256 : 128;
-  static constexpr int IT = MAXT / (N * TPI) > 0 ? MAXT / (N * TPI) : 1;
+  // V2 / fp64: the smallest tile (entries) whose mode-2/3 tasks fill their
+  // warps to >= 93 % (n = 10: 3 entries = 150 of 160 threads, not 2 = 100 of
+  // 128), at most 384 threads; V0/V1: as many entries as fit MAXT threads
+  __host__ __device__ static constexpr int pick_it() {
+    if (ES == 4 && V != 2 && V != 3) return MAXT / (N * TPI) > 0 ? MAXT / (N * TPI) : 1;
+    int best = 1, best_idle = 1 << 30;
+    for (int it = 1; it * N * TPI <= 384 || it == 1; ++it) {
+      const int t = it * N * TPI, w = (t + 31) / 32 * 32;
+      const int idle = (w - t) * 1000 / w;  // per mille
+      if (idle * 100 <= 7 * 1000) return it;
+      if (idle < best_idle) {
+        best_idle = idle;
+        best = it;
+      }
+    }
+    return best;
+  }
+  static constexpr int IT = pick_it();
   static constexpr int NP = IT * N;           // planes per tile
   static constexpr int NTASK = NP * TPI;      // mode-2 and mode-3 tasks per tile
   static constexpr int THREADS = (NTASK + 31) / 32 * 32;
   static constexpr int NCOL = NP * N;         // mode-1 columns per tile
   static constexpr int CA = (NCOL + THREADS - 1) / THREADS;
   static constexpr int STAGES = V == 1 ? 1 : 2;
-  static constexpr int MINB = ES == 4 ? (V == 1 ? 4 : (V == 2 ? 6 : 3)) : (V == 1 ? 6 : 3);
+  // resident CTAs the register budget targets (~24 warps per SM)
+  static constexpr int MINB_AUTO = 768 / ((IT * N * TPI + 31) / 32 * 32) > 0 ? 768 / ((IT * N * TPI + 31) / 32 * 32) : 1;
+  static constexpr int MINB = V == 3 ? (ES == 4 ? 4 : 3)
+                                     : (ES == 4 ? (V == 1 ? 4 : (V == 2 ? MINB_AUTO : 3)) : (V == 1 ? MINB_AUTO : 3));
   static constexpr int VXR = vec_width(N, ES);  // column read width (elements)
   // planes are 16-byte multiples (even n): one cp.async.bulk per plane into a
   // padded plane stride. Otherwise (odd n) the tile's entries are contiguous
@@ -264,7 +287,18 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
     __syncthreads();
 
     // ---- mode 2: T2(I_q, j, P2) = sum_m T1(I_q, m, P2) B_r(j, m), in place
-    if (task_ok) {
+    if constexpr (R == 1) {  // one row: FFMA2 pairs columns j, j+1 (uniform B_r pair)
+      if (task_ok) {
+        T* pl = buf + (P2 / N) * ITEM + (P2 % N) * PS + q;
+        T acc[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) acc[j] = T(0);
+#pragma unroll kCwUnroll
+        for (int m = 0; m < N; ++m) axpy_pairs_c(acc, kc.bt + m * N, pl[m * N], N);
+#pragma unroll
+        for (int j = 0; j < N; ++j) pl[j * N] = acc[j];
+      }
+    } else if (task_ok) {
       T* pl = buf + (P2 / N) * ITEM + (P2 % N) * PS + q * R;
       T acc[N][R];
 #pragma unroll
@@ -293,7 +327,20 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
     __syncthreads();
 
     // ---- mode 3: Y(I_q, j3, k) = init + sum_n T2(I_q, j3, n) Cw(k, n)
-    if (task_ok && e3 < valid) {
+    if constexpr (R == 1) {  // one row: FFMA2 pairs k, k+1 (uniform Cw pair)
+      if (task_ok && e3 < valid) {
+        const T* fb = buf + e3 * ITEM + j3 * N + q;
+        T* yb = p.Y + (first + e3) * p.sy + (long long)j3 * p.ldy + q;
+        T acc[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+          acc[k] = beta_mode == kBetaZero ? T(0) : beta_init(beta_mode, p.beta, yb[(long long)k * p.ldy2]);
+#pragma unroll kCwUnroll
+        for (int n = 0; n < N; ++n) axpy_pairs_c(acc, kc.ct + n * N, fb[n * PS], N);
+#pragma unroll
+        for (int k = 0; k < N; ++k) yb[(long long)k * p.ldy2] = acc[k];
+      }
+    } else if (task_ok && e3 < valid) {
       const bool two = N % 2 == 0 || q * R + 1 < N;
       const T* fb = buf + e3 * ITEM + j3 * N + q * R;
       T* yb = p.Y + (first + e3) * p.sy + (long long)j3 * p.ldy + q * R;
