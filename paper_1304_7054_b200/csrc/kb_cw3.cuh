@@ -66,7 +66,7 @@ struct Cw3 {
   // task -- twice the threads per entry (n = 16: 256), FFMA2 then pairs two
   // output COLUMNS with a uniform-register constant pair, like mode 1
   static constexpr int R = V == 3 ? 1 : 2;
-  static constexpr int TPI = (N + 1) / R;     // tasks per plane / per fiber column
+  static constexpr int TPI = (N + R - 1) / R;  // tasks per plane / per fiber column
   static constexpr int NN = N * N;
   // entries per tile: ~256 threads of mode-2/3 tasks (fp32, V0/V1), ~128
   // (fp64; fp32 V2: 4-warp CTAs, so each SM sub-partition interleaves warps

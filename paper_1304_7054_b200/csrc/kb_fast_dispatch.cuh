@@ -313,6 +313,7 @@ static int k3_family() {
   // odd n run the column-wise kernel with span loads)
   if (sizeof(T) == 4) return N == 8 ? 0 : ((N == 11 || N == 14) ? 1 : 3);
   if (N == 3 || N == 4) return 0;
+  if (N == 12 || N == 14) return 10;  // one row per task: fp64 n = 12 +15 %
   return (N <= 7 || N == 10) ? 1 : 2;
 }
 

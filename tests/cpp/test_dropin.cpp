@@ -141,7 +141,57 @@ void test_validation_messages() {
   CHECK(over);
 }
 
+// kron1 (kron1.hpp:17-62) and gemm_a (gemm_a.hpp:18-76) through the drop-in
+// headers with std::vector buffers, vs a double brute force.
+template <typename T>
+void test_kron1_gemm_a(int m, int batch) {
+  std::mt19937_64 g(777 + m);
+  const int n_a = m + 2;
+  auto a = rnd<T>(m * n_a, g), x = rnd<T>(n_a * batch, g), y = rnd<T>(m * batch, g);
+  const std::vector<T> y0 = y;
+  const T alpha = T(0.5), beta = T(-1.5);
+  kron1<T>(MatrixOp::NoTranspose, m, n_a, alpha, MatrixView<const T>(std::span<const T>(a), m, n_a, m),
+           BatchView<VectorView<const T>>(VectorView<const T>(std::span<const T>(x), n_a), batch, n_a), beta,
+           BatchView<VectorView<T>>(VectorView<T>(std::span<T>(y), m), batch, m));
+  const double tol = std::is_same_v<T, float> ? 1e-5 : 1e-12;
+  for (int p = 0; p < batch; p += std::max(1, batch / 9))
+    for (int i = 0; i < m; ++i) {
+      double w = beta * (double)y0[p * m + i];
+      for (int l = 0; l < n_a; ++l) w += alpha * (double)a[i + l * m] * (double)x[p * n_a + l];
+      CHECK(std::abs(w - (double)y[p * m + i]) <= tol * std::max(1.0, std::abs(w)) * 4);
+    }
+  // gemm_a, op(A) = A^T: A^p stored k x m
+  const int k = m + 1, n = 3;
+  auto A = rnd<T>(k * m * batch, g), B = rnd<T>(k * n, g), C = rnd<T>(m * n * batch, g);
+  const std::vector<T> C0 = C;
+  gemm_a<T>(MatrixOp::Transpose, MatrixOp::NoTranspose, m, n, k, alpha,
+            BatchView<MatrixView<const T>>(MatrixView<const T>(std::span<const T>(A), k, m, k), batch, k * m),
+            MatrixView<const T>(std::span<const T>(B), k, n, k), beta,
+            BatchView<MatrixView<T>>(MatrixView<T>(std::span<T>(C), m, n, m), batch, m * n));
+  for (int p = 0; p < batch; p += std::max(1, batch / 9))
+    for (int c = 0; c < n; ++c)
+      for (int i = 0; i < m; ++i) {
+        double w = beta * (double)C0[p * m * n + i + c * m];
+        for (int kk = 0; kk < k; ++kk) w += alpha * (double)A[p * k * m + kk + i * k] * (double)B[kk + c * k];
+        CHECK(std::abs(w - (double)C[p * m * n + i + c * m]) <= tol * std::max(1.0, std::abs(w)) * 4);
+      }
+  // reference error text (test_kron1.cpp:209-235)
+  bool threw = false;
+  try {
+    kron1<T>(MatrixOp::NoTranspose, m, n_a + 1, alpha, MatrixView<const T>(std::span<const T>(a), m, n_a, m),
+             BatchView<VectorView<const T>>(VectorView<const T>(std::span<const T>(x), n_a), batch, n_a), beta,
+             BatchView<VectorView<T>>(VectorView<T>(std::span<T>(y), m), batch, m));
+  } catch (const std::invalid_argument& e) {
+    threw = std::string(e.what()).find("kron1: A: op(A) is") == 0;
+  }
+  CHECK(threw);
+}
+
 int main() {
+  for (int m : {1, 5, 16, 24}) {
+    test_kron1_gemm_a<float>(m, 500);
+    test_kron1_gemm_a<double>(m, 200);
+  }
   for (int m : {1, 3, 10, 16}) {
     test_kron2<float>(m, 1000);
     test_kron2<double>(m, 300);
