@@ -1,4 +1,5 @@
+# One-call health check on a B200: GPU parity suite, smoke, bench line.
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -4
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()"
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
