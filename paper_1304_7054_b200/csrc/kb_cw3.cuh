@@ -76,6 +76,7 @@ struct Cw3 {
   // warps to >= 93 % (n = 10: 3 entries = 150 of 160 threads, not 2 = 100 of
   // 128), at most 384 threads; V0/V1: as many entries as fit MAXT threads
   __host__ __device__ static constexpr int pick_it() {
+    if (V == 4) return 1;  // one entry per CTA: CTA barriers span only that entry's warps
     if (ES == 4 && V != 2 && V != 3) return MAXT / (N * TPI) > 0 ? MAXT / (N * TPI) : 1;
     int best = 1, best_idle = 1 << 30;
     for (int it = 1; it * N * TPI <= 384 || it == 1; ++it) {
@@ -98,7 +99,8 @@ struct Cw3 {
   static constexpr int STAGES = V == 1 ? 1 : 2;
   // resident CTAs the register budget targets (~24 warps per SM)
   static constexpr int MINB_AUTO = 768 / ((IT * N * TPI + 31) / 32 * 32) > 0 ? 768 / ((IT * N * TPI + 31) / 32 * 32) : 1;
-  static constexpr int MINB = V == 3 ? (ES == 4 ? 4 : 3)
+  static constexpr int MINB = V == 4 ? MINB_AUTO
+                             : V == 3 ? (ES == 4 ? 4 : 3)
                                      : (ES == 4 ? (V == 1 ? 4 : (V == 2 ? MINB_AUTO : 3)) : (V == 1 ? MINB_AUTO : 3));
   static constexpr int VXR = vec_width(N, ES);  // column read width (elements)
   // planes are 16-byte multiples (even n): one cp.async.bulk per plane into a

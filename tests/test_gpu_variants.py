@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("env", [{"KB_YSTAGE": "1"}, {"KB_YSTAGE": "0"}] + [{"KB_K3": str(f)} for f in (0, 1, 2, 3, 9, 10)] + [{"KB_K2": str(f)} for f in range(3)])
+@pytest.mark.parametrize("env", [{"KB_YSTAGE": "1"}, {"KB_YSTAGE": "0"}] + [{"KB_K3": str(f)} for f in (0, 1, 2, 3, 9, 10, 11)] + [{"KB_K2": str(f)} for f in range(3)])
 def test_kernel_switches_bitwise(env):
     r = subprocess.run([sys.executable, os.path.join(HERE, "variant_check.py")], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
