@@ -41,6 +41,8 @@ METRIC = "batched Kron GFlop/s + HBM GB/s (n=16 fp32 2-D & 3-D) at 1/2/4/8 B200"
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
 FP32_PEAK_TFLOPS = 72.5    # measured FFMA peak (tools/microbench/fma_tput.cu, profiles/)
 FP64_PEAK_TFLOPS = 33.6    # measured DFMA peak
+FFMA2_PEAK_TFLOPS = 67.1   # measured fma.rn.f32x2 (FFMA2) peak -- the instruction the fp32 kernels issue
+                           # (profiles/r01_fma_tput.txt); reported beside, never as, the roofline
 
 WORKLOADS = {
     # name: (dims3, n, dtype, batch per GPU)
@@ -370,6 +372,8 @@ def main():
                    "ms_per_step": round(xms, 4), "hbm_gbs": round(gb, 1), "kernel": xpath,
                    "roofline": {"bound": "hbm" if roof_tf < fpeak else "fp-pipe", "roof_tflops": round(roof_tf, 2),
                                 "frac": round(tf / roof_tf, 4), "hbm_frac": round(gb / hbm_peak, 4)}}
+            if dt == "f32" and roof_tf >= fpeak:
+                rec["roofline"]["ffma2_peak_frac"] = round(tf / FFMA2_PEAK_TFLOPS, 4)
             if bt * be < (256 << 20):  # small batch: host launch cost dominates -> also report a CUDA-graph replay
                 gms = time_graph(kb, torch, name, max(20, args.steps), world)
                 rec["cuda_graph"] = {"ms_per_launch": round(gms, 4),
