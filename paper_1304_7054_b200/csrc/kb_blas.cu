@@ -11,7 +11,9 @@
 //          acc = sum_kk A^p(kk, i) B_r(kk, c) from 0, then
 //          fma(alpha, acc, beta == 0 ? 0 : fl(beta C)).
 //
-// Both are HBM-bound streaming operators (AI ~ n/4 .. n/2 flop/B): one thread
+// Both are HBM-bound streaming operators (AI ~ n/4 .. n/2 flop/B). kron1 at
+// square n <= 16 with contiguous entries runs kron1_sq_kernel (below); the
+// general kernels use one thread
 // per output element, consecutive threads on consecutive rows of one entry so
 // the per-entry operand reads broadcast through L1 and the output writes are
 // coalesced; the shared matrix is read through the read-only path (it stays
@@ -64,6 +66,86 @@ __global__ void gemm_a_kernel(const T* __restrict__ A, long long lda, long long 
   }
 }
 
+// ---- kron1, square n <= 16 with contiguous entries: one thread per entry.
+// A warp stages its 32 entries' x through smem with coalesced loads (odd
+// element stride, so the per-lane reads are conflict-free), each lane forms
+// y = init + A_r fl(alpha x) with A_r column pairs from the constant bank
+// (FFMA2 R.F32 x UR.F32x2 -- two rows, one scalar), and the warp writes the
+// results back coalesced.
+template <typename T, int N>
+struct K1Consts {
+  T a[N * N];  // a[i + l*N] = A_r(i, l)
+};
+
+template <typename T, int N>
+__global__ void __launch_bounds__(256) kron1_sq_kernel(const T* __restrict__ X, T* __restrict__ Y, long long batch,
+                                                       T alpha, int beta_mode, T beta,
+                                                       const __grid_constant__ K1Consts<T, N> kc) {
+  constexpr int SE = N % 2 ? N : N + 1;
+  __shared__ T sm[8][32 * SE];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T* s = sm[warp];
+  const long long ngroups = (batch + 31) / 32;
+  for (long long g = (long long)blockIdx.x * 8 + warp; g < ngroups; g += (long long)gridDim.x * 8) {
+    const long long first = g * 32;
+    const int valid = (int)(batch - first < 32 ? batch - first : 32);
+    for (int idx = lane; idx < valid * N; idx += 32) s[(idx / N) * SE + idx % N] = X[first * N + idx];
+    __syncwarp();
+    if (lane < valid) {
+      T acc[N];
+      const T* yp = Y + (first + lane) * N;
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = beta_mode == kBetaZero ? T(0) : beta_init(beta_mode, beta, yp[i]);
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        const T w = mul_rn(alpha, s[lane * SE + l]);
+        if constexpr (sizeof(T) == 4) {
+#pragma unroll
+          for (int i = 0; i + 1 < N; i += 2) {
+            const float2 d = ffma2_s(make_float2(kc.a[i + l * N], kc.a[i + 1 + l * N]), w,
+                                     make_float2(acc[i], acc[i + 1]));
+            acc[i] = d.x;
+            acc[i + 1] = d.y;
+          }
+          if constexpr (N % 2) acc[N - 1] = fma_rn(kc.a[N - 1 + l * N], w, acc[N - 1]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < N; ++i) acc[i] = fma_rn(kc.a[i + l * N], w, acc[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) s[lane * SE + i] = acc[i];  // this lane's own slot: no cross-lane hazard
+    }
+    __syncwarp();
+    for (int idx = lane; idx < valid * N; idx += 32) Y[first * N + idx] = s[(idx / N) * SE + idx % N];
+    __syncwarp();
+  }
+}
+
+template <typename T, int N>
+static cudaError_t launch_kron1_sq_n(const T* ha, const T* X, T* Y, long long batch, T alpha, int beta_mode, T beta,
+                                     int sm_count, cudaStream_t s) {
+  K1Consts<T, N> kc;
+  for (int i = 0; i < N * N; ++i) kc.a[i] = ha[i];
+  const long long want = ((batch + 31) / 32 + 7) / 8;
+  const int grid = (int)(want < (long long)sm_count * 8 ? want : (long long)sm_count * 8);
+  kron1_sq_kernel<T, N><<<grid > 0 ? grid : 1, 256, 0, s>>>(X, Y, batch, alpha, beta_mode, beta, kc);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_kron1_sq(int n, const T* ha, const T* X, T* Y, long long batch, T alpha, int beta_mode, T beta,
+                            int sm_count, cudaStream_t s) {
+  switch (n) {
+#define KB_K1(N) \
+  case N: return launch_kron1_sq_n<T, N>(ha, X, Y, batch, alpha, beta_mode, beta, sm_count, s);
+    KB_K1(1) KB_K1(2) KB_K1(3) KB_K1(4) KB_K1(5) KB_K1(6) KB_K1(7) KB_K1(8)
+    KB_K1(9) KB_K1(10) KB_K1(11) KB_K1(12) KB_K1(13) KB_K1(14) KB_K1(15) KB_K1(16)
+#undef KB_K1
+    default: return cudaErrorNotSupported;
+  }
+}
+
 template <typename T>
 cudaError_t launch_kron1(const T* A, long long lda, int opa, const T* X, long long sx, T* Y, long long sy,
                          long long m, long long n, long long batch, T alpha, int beta_mode, T beta, int sm_count,
@@ -89,6 +171,10 @@ cudaError_t launch_gemm_a(const T* A, long long lda, long long sa, int opa, cons
   return cudaGetLastError();
 }
 
+template cudaError_t launch_kron1_sq<float>(int, const float*, const float*, float*, long long, float, int, float, int,
+                                            cudaStream_t);
+template cudaError_t launch_kron1_sq<double>(int, const double*, const double*, double*, long long, double, int, double,
+                                             int, cudaStream_t);
 template cudaError_t launch_kron1<float>(const float*, long long, int, const float*, long long, float*, long long,
                                          long long, long long, long long, float, int, float, int, cudaStream_t);
 template cudaError_t launch_kron1<double>(const double*, long long, int, const double*, long long, double*, long long,

@@ -39,6 +39,10 @@ template <typename T>
 cudaError_t launch_kron1(const T* A, long long lda, int opa, const T* X, long long sx, T* Y, long long sy,
                          long long m, long long n, long long batch, T alpha, int beta_mode, T beta, int sm_count,
                          cudaStream_t s);
+// kron1 square n <= 16, contiguous x / y entries, host-resolved A_r (col-major).
+template <typename T>
+cudaError_t launch_kron1_sq(int n, const T* ha, const T* X, T* Y, long long batch, T alpha, int beta_mode, T beta,
+                            int sm_count, cudaStream_t s);
 template <typename T>
 cudaError_t launch_gemm_a(const T* A, long long lda, long long sa, int opa, const T* B, long long ldb, int opb, T* Cm,
                           long long ldc, long long sc, long long m, long long n, long long k, long long batch, T alpha,

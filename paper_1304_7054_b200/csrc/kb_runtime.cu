@@ -552,13 +552,21 @@ int kron1_entry(char ta, i64 m_a, i64 n_a, i64 batch, T alpha, const T* A, i64 l
     cudaStream_t us = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
     const bool sync = !(exec && (exec->flags & KB_EXEC_ASYNC) && (x_dev || scale_only) && y_dev);
     const int bmode = beta_mode_of((double)beta);
+    // square n <= 16 with contiguous entries: thread-per-entry kernel with A_r
+    // as a kernel parameter (no device copy of A)
+    const bool square_fast = m_a == n_a && m_a <= 16 && ldxp == n_a && ldyp == m_a;
     auto slice = [&](int dev, i64 p0, i64 p1) {
       const T* Ad = nullptr;
+      std::vector<T> ha;
       run_slice(
           dev, X, Y, p0, p1, sp, x_dev && xi.dev == dev, y_dev && yi.dev == dev, us, sync,
           [&](DevRes& r, cudaStream_t s) {
             if (scale_only) return;  // A, X never read (kron1.hpp:45-55)
             const i64 fa = fp_matrix(ac, lda);
+            if (square_fast) {
+              ha = resolve_sq(fetch_host(A, fa, s), lda, is_t(ta), (int)m_a, false, T(1), false);
+              return;
+            }
             T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + 32)));
             Ad = const_on_device(A, fa, r.device, cs, s);
           },
@@ -568,6 +576,11 @@ int kron1_entry(char ta, i64 m_a, i64 n_a, i64 batch, T alpha, const T* A, i64 l
               cuda_check(kb::launch_scale<T>(static_cast<T*>(yd), n, m_a, 1, 1, m_a, 0, ldyp, bmode, beta, grid, s),
                          "kron1");
               count_launch("scale");
+            } else if (square_fast) {
+              cuda_check(kb::launch_kron1_sq<T>((int)m_a, ha.data(), static_cast<const T*>(xd), static_cast<T*>(yd), n,
+                                                alpha, bmode, beta, r.sm_count, s),
+                         "kron1");
+              count_launch("kron1");
             } else {
               cuda_check(kb::launch_kron1<T>(Ad, lda, is_t(ta), static_cast<const T*>(xd), ldxp, static_cast<T*>(yd),
                                              ldyp, m_a, n_a, n, alpha, bmode, beta, r.sm_count, s),
