@@ -47,7 +47,6 @@ constexpr int XSLOTS = 2;                 // X entry buffers per group
 constexpr int XBYTES = N * N * N * 4;     // 16 KiB per entry
 constexpr int BBYTES = 32 * 32 * 4;       // one constant operand tile
 constexpr int EPAD = 20;                  // exchange row pitch (floats)
-constexpr int EBYTES = N * N * EPAD * 4;  // T2 exchange buffer per group
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int GCOLS = 128;                // TMEM columns per group
 // idesc: f32 accumulate, tf32 A/B, K-major A/B, N = 32, M = 128
