@@ -75,7 +75,18 @@ struct Cw3 {
   // V2 / fp64: the smallest tile (entries) whose mode-2/3 tasks fill their
   // warps to >= 93 % (n = 10: 3 entries = 150 of 160 threads, not 2 = 100 of
   // 128), at most 384 threads; V0/V1: as many entries as fit MAXT threads
+  // V6 "warp-plane": each warp owns PPW whole planes for modes 1 AND 2, so the
+  // mode-1 -> mode-2 dependency is intra-warp (__syncwarp); tiles hold the
+  // fewest entries whose planes split evenly over warps (n = 10: 6 planes per
+  // warp, 3 entries = 5 warps)
+  static constexpr bool WP = V == 6;
+  static constexpr int PPW = 32 / TPI > 0 ? 32 / TPI : 1;
   __host__ __device__ static constexpr int pick_it() {
+    if (V == 6) {
+      for (int it = 1; it <= 32; ++it)
+        if ((it * N) % PPW == 0 && it * N / PPW <= 12) return it;
+      return 1;
+    }
     if (V == 4) return 1;  // one entry per CTA: CTA barriers span only that entry's warps
     if (ES == 4 && V != 2 && V != 3) return MAXT / (N * TPI) > 0 ? MAXT / (N * TPI) : 1;
     int best = 1, best_idle = 1 << 30;
@@ -93,13 +104,14 @@ struct Cw3 {
   static constexpr int IT = pick_it();
   static constexpr int NP = IT * N;           // planes per tile
   static constexpr int NTASK = NP * TPI;      // mode-2 and mode-3 tasks per tile
-  static constexpr int THREADS = (NTASK + 31) / 32 * 32;
+  static constexpr int THREADS = WP ? (NP + PPW - 1) / PPW * 32 : (NTASK + 31) / 32 * 32;
   static constexpr int NCOL = NP * N;         // mode-1 columns per tile
-  static constexpr int CA = (NCOL + THREADS - 1) / THREADS;
+  static constexpr int CA = WP ? (PPW * N + 31) / 32 : (NCOL + THREADS - 1) / THREADS;
   static constexpr int STAGES = V == 1 ? 1 : 2;
   // resident CTAs the register budget targets (~24 warps per SM)
   static constexpr int MINB_AUTO = 768 / ((IT * N * TPI + 31) / 32 * 32) > 0 ? 768 / ((IT * N * TPI + 31) / 32 * 32) : 1;
-  static constexpr int MINB = V == 4 ? MINB_AUTO
+  static constexpr int MINB = V == 6 ? (768 / THREADS > 0 ? 768 / THREADS : 1)
+                             : V == 4 ? MINB_AUTO
                              : V == 3 ? (ES == 4 ? 4 : 3)
                                      : (ES == 4 ? (V == 1 ? 4 : (V == 2 ? MINB_AUTO : 3)) : (V == 1 ? MINB_AUTO : 3));
   static constexpr int VXR = vec_width(N, ES);  // column read width (elements)
@@ -131,7 +143,7 @@ struct Cw3 {
     {
       const int lanes = 128 / (VXR * ES) < 32 ? 128 / (VXR * ES) : 32;
       auto off = [&](int k) {
-        const int P = k % NP, m = k / NP;
+        const int P = WP ? k % PPW : k % NP, m = WP ? k / PPW : k / NP;
         return ((P / N) * item + (P % N) * ps + m * N) * wpe;
       };
       const int c = phase_banks(off, lanes, VXR * wpe);
@@ -141,7 +153,7 @@ struct Cw3 {
     {
       const int lanes = 128 / (VR * ES) < 32 ? 128 / (VR * ES) : 32;
       auto off = [&](int k) {
-        const int P = plane_of_group(k / TPI), q = k % TPI;
+        const int P = WP ? k / TPI : plane_of_group(k / TPI), q = k % TPI;
         return ((P / N) * item + (P % N) * ps + q * R) * wpe;
       };
       const int c = phase_banks(off, lanes, VR * wpe);
@@ -226,8 +238,12 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
   // per-thread task coordinates (fixed for the kernel)
   const bool task_ok = tid < K::NTASK;
   const int q = tid % TPI;
-  const int P2 = K::plane_of_group(tid / TPI);                  // mode-2 plane (entry-major)
   const int j3 = (tid / TPI) % N, e3 = tid / (TPI * N);        // mode-3 fiber column / entry
+  const int wid = tid >> 5, lid = tid & 31;
+  // mode-2 task: warp-plane (V6) = this warp's planes, else entry-major groups
+  const bool m2_ok = K::WP ? (lid < K::PPW * TPI && wid * K::PPW + lid / TPI < NP) : task_ok;
+  const int P2 = K::WP ? wid * K::PPW + lid / TPI : K::plane_of_group(tid / TPI);
+  const int q2 = K::WP ? lid % TPI : q;
 
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) issue(blockIdx.x + (long long)s * gridDim.x, s);
@@ -248,10 +264,21 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
     {
       T acc[K::CA][N];
       T* col[K::CA];
+      bool cok[K::CA];
 #pragma unroll
       for (int k = 0; k < K::CA; ++k) {
-        const int c = tid + k * K::THREADS;
-        const int P = c % NP, m = c / NP;
+        int P, m;
+        if constexpr (K::WP) {
+          const int c = lid + 32 * k;
+          P = wid * K::PPW + c % K::PPW;
+          m = c / K::PPW;
+          cok[k] = c < K::PPW * N && P < NP;
+        } else {
+          const int c = tid + k * K::THREADS;
+          P = c % NP;
+          m = c / NP;
+          cok[k] = K::CA * K::THREADS == K::NCOL || c < K::NCOL;
+        }
         col[k] = buf + (P / N) * ITEM + (P % N) * PS + m * N;
 #pragma unroll
         for (int i = 0; i < N; ++i) acc[k][i] = T(0);
@@ -261,7 +288,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
         T x[K::CA][K::VXR];
 #pragma unroll
         for (int k = 0; k < K::CA; ++k)
-          if (K::CA * K::THREADS == K::NCOL || tid + k * K::THREADS < K::NCOL) lds_vec<K::VXR>(x[k], col[k] + l0);
+          if (cok[k]) lds_vec<K::VXR>(x[k], col[k] + l0);
 #pragma unroll
         for (int ll = 0; ll < K::VXR; ++ll)
 #pragma unroll
@@ -269,7 +296,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
       }
 #pragma unroll
       for (int k = 0; k < K::CA; ++k)
-        if (K::CA * K::THREADS == K::NCOL || tid + k * K::THREADS < K::NCOL)
+        if (cok[k])
 #pragma unroll
           for (int i = 0; i < N; i += K::VXR) {
             T v[K::VXR];
@@ -286,12 +313,15 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
               for (int u = 0; u < K::VXR; ++u) col[k][i + u] = v[u];
           }
     }
-    __syncthreads();
+    if constexpr (K::WP)
+      __syncwarp();  // this warp's planes are complete in T1
+    else
+      __syncthreads();
 
     // ---- mode 2: T2(I_q, j, P2) = sum_m T1(I_q, m, P2) B_r(j, m), in place
     if constexpr (R == 1) {  // one row: FFMA2 pairs columns j, j+1 (uniform B_r pair)
-      if (task_ok) {
-        T* pl = buf + (P2 / N) * ITEM + (P2 % N) * PS + q;
+      if (m2_ok) {
+        T* pl = buf + (P2 / N) * ITEM + (P2 % N) * PS + q2;
         T acc[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) acc[j] = T(0);
@@ -300,8 +330,8 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
 #pragma unroll
         for (int j = 0; j < N; ++j) pl[j * N] = acc[j];
       }
-    } else if (task_ok) {
-      T* pl = buf + (P2 / N) * ITEM + (P2 % N) * PS + q * R;
+    } else if (m2_ok) {
+      T* pl = buf + (P2 / N) * ITEM + (P2 % N) * PS + q2 * R;
       T acc[N][R];
 #pragma unroll
       for (int j = 0; j < N; ++j)
@@ -322,7 +352,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
           *reinterpret_cast<double2*>(pl + j * N) = make_double2(acc[j][0], acc[j][1]);
         else {
           pl[j * N] = acc[j][0];
-          if (N % 2 == 0 || q * R + 1 < N) pl[j * N + 1] = acc[j][1];  // odd n: last task owns one row
+          if (N % 2 == 0 || q2 * R + 1 < N) pl[j * N + 1] = acc[j][1];  // odd n: last task owns one row
         }
       }
     }

@@ -303,16 +303,17 @@ static cudaError_t launch3tiny(const Kron3Params<T>& p, const T* ha, const T* hb
 // early stage release (1 / 2 stages); n <= 4 tight entries first try the
 // tiny-entry kernel (9 forces it; any other KB_K3 skips it), 10 = column-wise
 // with one row per mode-2/3 task (2x threads per entry), 11 = column-wise
-// with one entry per CTA. KB_K3 overrides
+// with one entry per CTA, 13 = column-wise warp-plane (each warp owns whole
+// planes for modes 1 and 2: no CTA barrier between them). KB_K3 overrides
 // the default for sweeps.
 template <typename T, int N>
 static int k3_family() {
   static const int force = env_variant("KB_K3", -1);
   if (N < 3) return 0;
-  if (force >= 0) return N % 2 && force > 3 && force != 11 ? 0 : force;
+  if (force >= 0) return N % 2 && force > 3 && force != 11 && force != 13 ? 0 : force;
   // fastest family per size, measured on B200 (profiles/r01_k3_families.txt;
   // odd n run the column-wise kernel with span loads)
-  if (sizeof(T) == 4) return N == 8 ? 0 : ((N == 11 || N == 14) ? 1 : 3);
+  if (sizeof(T) == 4) return N == 8 ? 0 : N == 9 ? 13 : ((N == 11 || N == 14) ? 1 : 3);  // n = 9 warp-plane: +9 %
   if (N == 3 || N == 4) return 0;
   if (N == 12 || N == 14) return 10;  // one row per task: fp64 n = 12 +15 %
   if (N == 10) return 11;              // one entry per CTA: +3 %
@@ -349,12 +350,13 @@ static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, co
       }
     }
 #endif
-    if ((fam >= 1 && fam <= 3) || fam == 10 || fam == 11) {
+    if ((fam >= 1 && fam <= 3) || fam == 10 || fam == 11 || fam == 13) {
       const cudaError_t e = fam == 1    ? launch3cw<T, N, 0>(p, ha, hb, hc, sm_count, s)
                             : fam == 2  ? launch3cw<T, N, 1>(p, ha, hb, hc, sm_count, s)
                             : fam == 3  ? launch3cw<T, N, 2>(p, ha, hb, hc, sm_count, s)
                             : fam == 10 ? launch3cw<T, N, 3>(p, ha, hb, hc, sm_count, s)
-                                        : launch3cw<T, N, 4>(p, ha, hb, hc, sm_count, s);
+                            : fam == 11 ? launch3cw<T, N, 4>(p, ha, hb, hc, sm_count, s)
+                                        : launch3cw<T, N, 6>(p, ha, hb, hc, sm_count, s);
       if (e != cudaErrorNotSupported) return e;
     }
   }
