@@ -35,9 +35,12 @@ constexpr int kCwUnroll = KB_CW_UNROLL;
 
 template <typename T, int N>
 struct SqConstsCw3 {
-  T a[N * N];   // a[l*N + i]  = A_r(i, l)          (column l contiguous: row pairs)
-  T bt[N * N];  // bt[m*N + j] = B_r(j, m)          (all j of one m contiguous)
-  T ct[N * N];  // ct[n*N + k] = fl(alpha*C_r(k, n))
+  // column stride: even, so every row pair {i, i+1} (i even) of every column is
+  // an 8-byte-aligned constant-bank pair (one UR.F32x2 FFMA2 operand, no UMOVs)
+  static constexpr int LD = N % 2 ? N + 1 : N;
+  T a[N * LD];   // a[l*LD + i]  = A_r(i, l)          (column l contiguous: row pairs)
+  T bt[N * LD];  // bt[m*LD + j] = B_r(j, m)          (all j of one m contiguous)
+  T ct[N * LD];  // ct[n*LD + k] = fl(alpha*C_r(k, n))
 };
 
 // Bank multiplicity of one shared-memory access phase: `lanes` lanes, lane k at
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
 #pragma unroll
         for (int ll = 0; ll < K::VXR; ++ll)
 #pragma unroll
-          for (int k = 0; k < K::CA; ++k) axpy_pairs_c(acc[k], kc.a + (l0 + ll) * N, x[k][ll], N);
+          for (int k = 0; k < K::CA; ++k) axpy_pairs_c(acc[k], kc.a + (l0 + ll) * kc.LD, x[k][ll], N);
       }
 #pragma unroll
       for (int k = 0; k < K::CA; ++k)
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
 #pragma unroll
         for (int j = 0; j < N; ++j) acc[j] = T(0);
 #pragma unroll kCwUnroll
-        for (int m = 0; m < N; ++m) axpy_pairs_c(acc, kc.bt + m * N, pl[m * N], N);
+        for (int m = 0; m < N; ++m) axpy_pairs_c(acc, kc.bt + m * kc.LD, pl[m * N], N);
 #pragma unroll
         for (int j = 0; j < N; ++j) pl[j * N] = acc[j];
       }
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
         T t[R];
         lds_n<R, K::VR>(t, pl + m * N);
 #pragma unroll
-        for (int j = 0; j < N; ++j) axpy_rows<R>(acc[j], t, kc.bt[m * N + j]);
+        for (int j = 0; j < N; ++j) axpy_rows<R>(acc[j], t, kc.bt[m * kc.LD + j]);
       }
 #pragma unroll
       for (int j = 0; j < N; ++j) {
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
         for (int k = 0; k < N; ++k)
           acc[k] = beta_mode == kBetaZero ? T(0) : beta_init(beta_mode, p.beta, yb[(long long)k * p.ldy2]);
 #pragma unroll kCwUnroll
-        for (int n = 0; n < N; ++n) axpy_pairs_c(acc, kc.ct + n * N, fb[n * PS], N);
+        for (int n = 0; n < N; ++n) axpy_pairs_c(acc, kc.ct + n * kc.LD, fb[n * PS], N);
 #pragma unroll
         for (int k = 0; k < N; ++k) yb[(long long)k * p.ldy2] = acc[k];
       }
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
         T f[R];
         lds_n<R, K::VR>(f, fb + n * PS);
 #pragma unroll
-        for (int k = 0; k < N; ++k) axpy_rows<R>(acc[k], f, kc.ct[n * N + k]);
+        for (int k = 0; k < N; ++k) axpy_rows<R>(acc[k], f, kc.ct[n * kc.LD + k]);
       }
 #pragma unroll
       for (int k = 0; k < N; ++k) {
@@ -517,8 +520,8 @@ __global__ void __launch_bounds__(128, Cwp3<T, S, EARLY>::MINB)
         lds_vec<VXR>(x1, c1 + l0);
 #pragma unroll
         for (int ll = 0; ll < VXR; ++ll) {
-          axpy_pairs_c(acc0, kc.a + (l0 + ll) * N, x0[ll], N);
-          axpy_pairs_c(acc1, kc.a + (l0 + ll) * N, x1[ll], N);
+          axpy_pairs_c(acc0, kc.a + (l0 + ll) * kc.LD, x0[ll], N);
+          axpy_pairs_c(acc1, kc.a + (l0 + ll) * kc.LD, x1[ll], N);
         }
       }
 #pragma unroll
@@ -545,7 +548,7 @@ __global__ void __launch_bounds__(128, Cwp3<T, S, EARLY>::MINB)
         T t[R];
         lds_vec<VR>(t, pl + m * N);
 #pragma unroll
-        for (int j = 0; j < N; ++j) axpy_rows<R>(acc[j], t, kc.bt[m * N + j]);
+        for (int j = 0; j < N; ++j) axpy_rows<R>(acc[j], t, kc.bt[m * kc.LD + j]);
       }
 #pragma unroll
       for (int j = 0; j < N; ++j) {
@@ -593,14 +596,14 @@ __global__ void __launch_bounds__(128, Cwp3<T, S, EARLY>::MINB)
 #pragma unroll
         for (int n = 0; n < N; ++n)
 #pragma unroll
-          for (int k = 0; k < N; ++k) axpy_rows<R>(acc[k], f[n], kc.ct[n * N + k]);
+          for (int k = 0; k < N; ++k) axpy_rows<R>(acc[k], f[n], kc.ct[n * kc.LD + k]);
       } else {
 #pragma unroll
         for (int n = 0; n < N; ++n) {
           T f[R];
           lds_vec<VR>(f, fb + n * PS);
 #pragma unroll
-          for (int k = 0; k < N; ++k) axpy_rows<R>(acc[k], f, kc.ct[n * N + k]);
+          for (int k = 0; k < N; ++k) axpy_rows<R>(acc[k], f, kc.ct[n * kc.LD + k]);
         }
       }
 #pragma unroll
@@ -700,8 +703,8 @@ __global__ void __launch_bounds__(128, Cwpp3<T>::MINB)
         lds_vec<VXR>(x1, c1 + l0);
 #pragma unroll
         for (int ll = 0; ll < VXR; ++ll) {
-          axpy_pairs_c(acc0, kc.a + (l0 + ll) * N, x0[ll], N);
-          axpy_pairs_c(acc1, kc.a + (l0 + ll) * N, x1[ll], N);
+          axpy_pairs_c(acc0, kc.a + (l0 + ll) * kc.LD, x0[ll], N);
+          axpy_pairs_c(acc1, kc.a + (l0 + ll) * kc.LD, x1[ll], N);
         }
       }
 #pragma unroll
@@ -726,7 +729,7 @@ __global__ void __launch_bounds__(128, Cwpp3<T>::MINB)
         T t[R];
         lds_vec<VR>(t, pl + m * N);
 #pragma unroll
-        for (int j = 0; j < N; ++j) axpy_rows<R>(acc[j], t, kc.bt[m * N + j]);
+        for (int j = 0; j < N; ++j) axpy_rows<R>(acc[j], t, kc.bt[m * kc.LD + j]);
       }
 #pragma unroll
       for (int j = 0; j < N; ++j) {
@@ -766,7 +769,7 @@ __global__ void __launch_bounds__(128, Cwpp3<T>::MINB)
         T f[R];
         lds_vec<VR>(f, fb + n * PS);
 #pragma unroll
-        for (int kk = 0; kk < N; ++kk) axpy_rows<R>(acc[kk], f, kc.ct[n * N + kk]);
+        for (int kk = 0; kk < N; ++kk) axpy_rows<R>(acc[kk], f, kc.ct[n * kc.LD + kk]);
       }
 #pragma unroll
       for (int kk = 0; kk < N; ++kk) stg_n<R, VR>(yb + (long long)kk * p.ldy2, acc[kk]);

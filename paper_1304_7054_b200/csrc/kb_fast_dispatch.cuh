@@ -211,9 +211,9 @@ static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, 
   SqConstsCw3<T, N> kc;
   for (int i = 0; i < N; ++i)
     for (int j = 0; j < N; ++j) {
-      kc.a[i + j * N] = ha[i + j * N];
-      kc.bt[j * N + i] = hb[i * N + j];  // bt[m*N + j] = B_r(j, m)
-      kc.ct[j * N + i] = hc[i * N + j];  // ct[n*N + k] = Cw(k, n)
+      kc.a[i + j * kc.LD] = ha[i + j * N];
+      kc.bt[j * kc.LD + i] = hb[i * N + j];  // bt[m*LD + j] = B_r(j, m)
+      kc.ct[j * kc.LD + i] = hc[i * N + j];  // ct[n*LD + k] = Cw(k, n)
     }
   kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
   return cudaGetLastError();
@@ -237,9 +237,9 @@ static cudaError_t launch3cwp(const Kron3Params<T>& p, const T* ha, const T* hb,
   SqConstsCw3<T, N> kc;
   for (int i = 0; i < N; ++i)
     for (int j = 0; j < N; ++j) {
-      kc.a[i + j * N] = ha[i + j * N];
-      kc.bt[j * N + i] = hb[i * N + j];
-      kc.ct[j * N + i] = hc[i * N + j];
+      kc.a[i + j * kc.LD] = ha[i + j * N];
+      kc.bt[j * kc.LD + i] = hb[i * N + j];
+      kc.ct[j * kc.LD + i] = hc[i * N + j];
     }
   kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
   return cudaGetLastError();
@@ -262,9 +262,9 @@ static cudaError_t launch3cwpp(const Kron3Params<T>& p, const T* ha, const T* hb
   SqConstsCw3<T, N> kc;
   for (int i = 0; i < N; ++i)
     for (int j = 0; j < N; ++j) {
-      kc.a[i + j * N] = ha[i + j * N];
-      kc.bt[j * N + i] = hb[i * N + j];
-      kc.ct[j * N + i] = hc[i * N + j];
+      kc.a[i + j * kc.LD] = ha[i + j * N];
+      kc.bt[j * kc.LD + i] = hb[i * N + j];
+      kc.ct[j * kc.LD + i] = hc[i * N + j];
     }
   kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
   return cudaGetLastError();
