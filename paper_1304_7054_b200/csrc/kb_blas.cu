@@ -11,9 +11,9 @@
 //          acc = sum_kk A^p(kk, i) B_r(kk, c) from 0, then
 //          fma(alpha, acc, beta == 0 ? 0 : fl(beta C)).
 //
-// Both are HBM-bound streaming operators (AI ~ n/4 .. n/2 flop/B). kron1 at
-// square n <= 16 with contiguous entries runs kron1_sq_kernel (below); the
-// general kernels use one thread
+// Both are HBM-bound streaming operators (AI ~ n/4 .. n/2 flop/B). At square
+// n <= 16 with contiguous entries kron1 runs kron1_sq_kernel and gemm_a
+// gemm_a_sq_kernel (below); the general kernels use one thread
 // per output element, consecutive threads on consecutive rows of one entry so
 // the per-entry operand reads broadcast through L1 and the output writes are
 // coalesced; the shared matrix is read through the read-only path (it stays
@@ -146,6 +146,180 @@ cudaError_t launch_kron1_sq(int n, const T* ha, const T* X, T* Y, long long batc
   }
 }
 
+// ---- gemm_a, square n <= 16 with tight entries (lda = n, entry stride n*n):
+// one thread per (entry, output column c). A CTA tile of E = 256/n entries is
+// copied to smem (fp64: element-granular cp.async, two stages, so the next
+// tile is in flight while this one computes; fp32: one stage, loads batched in
+// registers -- the faster choice per dtype), with op(A) resolved on the way in (column kk of
+// op(A) contiguous at an even stride CS, entries padded apart, so the row-pair
+// reads are 8-byte LDS that the n threads of one entry broadcast). Thread c
+// runs the reference's per-column order: op N (gemm_axpy) acc = init, then
+// acc_i = fma(op(A)(i, kk), w(kk, c), acc_i) with w = fl(alpha B_r) folded on
+// the host; op T (gemm_dot) acc from 0 with w = B_r, then fma(alpha, acc, init).
+// Rows pair into FFMA2 (two rows, one scalar). Results go back through the same
+// smem tile so the C stores are coalesced.
+template <typename T, int N>
+struct GaConsts {
+  T w[N * N];  // w[kk + c*N] = fl(alpha B_r(kk, c)) (op_a N) or B_r(kk, c) (op_a T)
+};
+
+template <typename T, int N>
+struct GaTile {
+  // column stride: fp32 a multiple of 4 (16-byte LDS of 4 rows), fp64 even;
+  // the pad shifts consecutive columns across banks for the op-T staging stores
+  static constexpr int CS = sizeof(T) == 4 ? (N % 4 == 0 ? N + 4 : (N + 3) / 4 * 4) : (N % 2 ? N + 1 : N + 2);
+  static constexpr int EST = (N * CS + 3) / 4 * 4 + 4;       // entry stride (16-B multiple, bank-shifted)
+  static constexpr int E = 256 / N;                           // entries per tile
+  // fp64: two cp.async stages (measured faster); fp32: one stage, register-batched loads
+  static constexpr bool PIPE = sizeof(T) == 8;
+  static constexpr int STAGES = PIPE ? 2 : 1;
+};
+
+template <typename T, int N, bool OPT>
+__global__ void __launch_bounds__(256) gemm_a_sq_kernel(const T* __restrict__ A, T* __restrict__ Cm, long long batch,
+                                                        T alpha, int beta_mode, T beta,
+                                                        const __grid_constant__ GaConsts<T, N> gc) {
+  using G = GaTile<T, N>;
+  constexpr int NN = N * N, CS = G::CS, EST = G::EST, E = G::E, TS = E * EST;
+  extern __shared__ __align__(16) unsigned char ga_smem[];
+  T* sa = reinterpret_cast<T*>(ga_smem);  // two stages of TS: tile t computes while tile t+1 lands
+  T* sw = sa + G::STAGES * TS;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NN; i += 256) sw[(i % N) * N + i / N] = gc.w[i];  // sw[kk*N + c]: lanes c read consecutive words
+  const int el = tid / N, c = tid % N;
+  const long long ntiles = (batch + E - 1) / E;
+  // element-granular async copies resolve op(A) on the way in: op N r = i + kk*N,
+  // op T r = kk + i*N (A^p(kk, i) = op(A)(i, kk)); always one commit group per call
+  auto issue = [&](long long tile, int st) {
+    if (tile < ntiles) {
+      const long long first = tile * E;
+      const int lim = (int)(batch - first < E ? batch - first : E) * NN;
+      const T* src = A + first * NN;
+      T* dst = sa + st * TS;
+#pragma unroll 4
+      for (int g = tid; g < lim; g += 256) {
+        const int e = g / NN, r = g - e * NN;
+        const int i = OPT ? r / N : r % N, kk = OPT ? r % N : r / N;
+        cp_async<sizeof(T)>(dst + e * EST + i + kk * CS, src + g, true);
+      }
+    }
+    cp_async_commit();
+  };
+  int st = 0;
+  if constexpr (G::PIPE) issue(blockIdx.x, 0);
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, st ^= (G::PIPE ? 1 : 0)) {
+    const long long first = tile * E;
+    const int valid = (int)(batch - first < E ? batch - first : E);
+    __syncthreads();  // the stage being refilled (previous output staging) is drained; sw is filled
+    if constexpr (G::PIPE) {
+      issue(tile + gridDim.x, st ^ 1);
+      cp_async_wait<1>();
+    } else {
+      // one stage: all of this thread's loads in flight before the first smem store
+      constexpr int LPT = (E * NN + 255) / 256;
+      const int lim = valid * NN;
+      const T* src = A + first * NN;
+      T v[LPT];
+#pragma unroll
+      for (int t = 0; t < LPT; ++t)
+        if (tid + t * 256 < lim) v[t] = __ldcs(src + tid + t * 256);
+#pragma unroll
+      for (int t = 0; t < LPT; ++t) {
+        const int g = tid + t * 256;
+        if (g < lim) {
+          const int e = g / NN, r = g - e * NN;
+          const int i = OPT ? r / N : r % N, kk = OPT ? r % N : r / N;
+          sa[e * EST + i + kk * CS] = v[t];
+        }
+      }
+    }
+    __syncthreads();  // this tile's op(A) is visible to every thread
+    T* sst = sa + st * TS;
+    T acc[N];
+    const bool act = el < valid;
+    T* cg = Cm + (first + el) * NN + c * N;  // column c of this thread's C entry
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = OPT || beta_mode == kBetaZero ? T(0) : beta_init(beta_mode, beta, cg[i]);
+      const T* ae = sst + el * EST;
+#pragma unroll
+      for (int kk = 0; kk < N; ++kk) {
+        const T w = sw[kk * N + c];
+        const T* col = ae + kk * CS;
+        if constexpr (sizeof(T) == 4) {
+          float a[(N + 3) / 4 * 4];
+#pragma unroll
+          for (int i = 0; i < N; i += 4) *reinterpret_cast<float4*>(a + i) = *reinterpret_cast<const float4*>(col + i);
+#pragma unroll
+          for (int i = 0; i + 1 < N; i += 2) {
+            const float2 d = ffma2_s(make_float2(a[i], a[i + 1]), w, make_float2(acc[i], acc[i + 1]));
+            acc[i] = d.x;
+            acc[i + 1] = d.y;
+          }
+          if constexpr (N % 2) acc[N - 1] = fma_rn(a[N - 1], w, acc[N - 1]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < N; ++i) acc[i] = fma_rn(col[i], w, acc[i]);
+        }
+      }
+      if constexpr (OPT) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const T init = beta_mode == kBetaZero ? T(0) : mul_rn(beta, cg[i]);
+          acc[i] = fma_rn(alpha, acc[i], init);
+        }
+      }
+    }
+    __syncthreads();  // every thread is done reading op(A) out of this stage
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) sst[el * EST + i + c * CS] = acc[i];
+    }
+    __syncthreads();
+    T* dst = Cm + first * NN;
+#pragma unroll 4
+    for (int g = tid; g < valid * NN; g += 256) {
+      const int e = g / NN, r = g - e * NN;
+      __stcs(dst + g, sst[e * EST + r % N + (r / N) * CS]);
+    }
+  }
+  if constexpr (G::PIPE) cp_async_wait<0>();
+}
+
+template <typename T, int N>
+static cudaError_t launch_gemm_a_sq_n(bool opt, const T* hw, const T* A, T* Cm, long long batch, T alpha,
+                                      int beta_mode, T beta, int sm_count, cudaStream_t s) {
+  GaConsts<T, N> gc;
+  for (int i = 0; i < N * N; ++i) gc.w[i] = hw[i];
+  const long long ntiles = (batch + GaTile<T, N>::E - 1) / GaTile<T, N>::E;
+  auto kern = opt ? gemm_a_sq_kernel<T, N, true> : gemm_a_sq_kernel<T, N, false>;
+  using G = GaTile<T, N>;
+  const size_t smem = sizeof(T) * ((size_t)G::STAGES * G::E * G::EST + N * N);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem) != cudaSuccess || occ < 1) occ = 1;
+  const long long cap = (long long)sm_count * occ;
+  const int grid = (int)(ntiles < cap ? ntiles : cap);
+  kern<<<grid > 0 ? grid : 1, 256, smem, s>>>(A, Cm, batch, alpha, beta_mode, beta, gc);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_gemm_a_sq(int n, bool opt, const T* hw, const T* A, T* Cm, long long batch, T alpha, int beta_mode,
+                             T beta, int sm_count, cudaStream_t s) {
+  switch (n) {
+#define KB_GA(N) \
+  case N: return launch_gemm_a_sq_n<T, N>(opt, hw, A, Cm, batch, alpha, beta_mode, beta, sm_count, s);
+    KB_GA(1) KB_GA(2) KB_GA(3) KB_GA(4) KB_GA(5) KB_GA(6) KB_GA(7) KB_GA(8)
+    KB_GA(9) KB_GA(10) KB_GA(11) KB_GA(12) KB_GA(13) KB_GA(14) KB_GA(15) KB_GA(16)
+#undef KB_GA
+    default: return cudaErrorNotSupported;
+  }
+}
+
 template <typename T>
 cudaError_t launch_kron1(const T* A, long long lda, int opa, const T* X, long long sx, T* Y, long long sy,
                          long long m, long long n, long long batch, T alpha, int beta_mode, T beta, int sm_count,
@@ -175,6 +349,10 @@ template cudaError_t launch_kron1_sq<float>(int, const float*, const float*, flo
                                             cudaStream_t);
 template cudaError_t launch_kron1_sq<double>(int, const double*, const double*, double*, long long, double, int, double,
                                              int, cudaStream_t);
+template cudaError_t launch_gemm_a_sq<float>(int, bool, const float*, const float*, float*, long long, float, int,
+                                             float, int, cudaStream_t);
+template cudaError_t launch_gemm_a_sq<double>(int, bool, const double*, const double*, double*, long long, double, int,
+                                              double, int, cudaStream_t);
 template cudaError_t launch_kron1<float>(const float*, long long, int, const float*, long long, float*, long long,
                                          long long, long long, long long, float, int, float, int, cudaStream_t);
 template cudaError_t launch_kron1<double>(const double*, long long, int, const double*, long long, double*, long long,

@@ -44,6 +44,9 @@ template <typename T>
 cudaError_t launch_kron1_sq(int n, const T* ha, const T* X, T* Y, long long batch, T alpha, int beta_mode, T beta,
                             int sm_count, cudaStream_t s);
 template <typename T>
+cudaError_t launch_gemm_a_sq(int n, bool opt, const T* hw, const T* A, T* Cm, long long batch, T alpha, int beta_mode,
+                             T beta, int sm_count, cudaStream_t s);
+template <typename T>
 cudaError_t launch_gemm_a(const T* A, long long lda, long long sa, int opa, const T* B, long long ldb, int opb, T* Cm,
                           long long ldc, long long sc, long long m, long long n, long long k, long long batch, T alpha,
                           int beta_mode, T beta, int sm_count, cudaStream_t s);

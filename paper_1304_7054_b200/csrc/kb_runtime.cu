@@ -626,13 +626,23 @@ int gemm_a_entry(char ta, char tb, i64 m, i64 n, i64 k, i64 batch, T alpha, cons
     cudaStream_t us = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
     const bool sync = !(exec && (exec->flags & KB_EXEC_ASYNC) && (a_dev || scale_only) && c_dev);
     const int bmode = beta_mode_of((double)beta);
+    // square n <= 16 with tight entries: thread-per-(entry, column) kernel with
+    // op(B) (scaled by alpha for op_a N) as a kernel parameter
+    static const bool generic_only = std::getenv("KB_GA_GENERIC") != nullptr;  // A/B switch for sweeps
+    const bool square_fast =
+        !generic_only && m == n && n == k && m <= 16 && lda == m && ldap == m * k && ldc == m && ldcp == m * n;
     auto slice = [&](int dev, i64 p0, i64 p1) {
       const T* Bd = nullptr;
+      std::vector<T> hw;
       run_slice(
           dev, A, Cm, p0, p1, sp, a_dev && ai.dev == dev, c_dev && ci.dev == dev, us, sync,
           [&](DevRes& r, cudaStream_t s) {
             if (scale_only) return;  // A, B never read (gemm_a.hpp:46-58)
             const i64 fb = fp_matrix(bc, ldb);
+            if (square_fast) {  // w(kk, c) = op(B)(kk, c), times alpha for gemm_axpy (detail.hpp:53)
+              hw = resolve_sq(fetch_host(B, fb, s), ldb, is_t(tb), (int)m, false, alpha, !is_t(ta));
+              return;
+            }
             T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fb + 32)));
             Bd = const_on_device(B, fb, r.device, cs, s);
           },
@@ -642,6 +652,11 @@ int gemm_a_entry(char ta, char tb, i64 m, i64 n, i64 k, i64 batch, T alpha, cons
               cuda_check(kb::launch_scale<T>(static_cast<T*>(cd), nb, m, n, 1, ldc, 0, ldcp, bmode, beta, grid, s),
                          "gemm_a");
               count_launch("scale");
+            } else if (square_fast) {
+              cuda_check(kb::launch_gemm_a_sq<T>((int)m, is_t(ta), hw.data(), static_cast<const T*>(ad),
+                                                 static_cast<T*>(cd), nb, alpha, bmode, beta, r.sm_count, s),
+                         "gemm_a");
+              count_launch("gemm_a");
             } else {
               cuda_check(kb::launch_gemm_a<T>(static_cast<const T*>(ad), lda, ldap, is_t(ta), Bd, ldb, is_t(tb),
                                               static_cast<T*>(cd), ldc, ldcp, m, n, k, nb, alpha, bmode, beta,

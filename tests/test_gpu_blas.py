@@ -77,7 +77,8 @@ def run_gemm_a(opa, opb, m, n, k, alpha, A, lda, sa, batch, B, ldb, beta, Cm, ld
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("m, n, k", [(1, 1, 1), (4, 3, 5), (16, 16, 16), (9, 20, 7), (33, 2, 19)])
+@pytest.mark.parametrize("m, n, k", [(1, 1, 1), (4, 3, 5), (5, 5, 5), (10, 10, 10), (13, 13, 13), (16, 16, 16), (9, 20, 7),
+                                     (33, 2, 19)])
 @pytest.mark.parametrize("opa, opb", [("N", "N"), ("N", "T"), ("T", "N"), ("T", "T")])
 @pytest.mark.parametrize("alpha, beta", [(1.0, 0.0), (0.75, 1.25)])
 def test_gemm_a_vs_oracle(dtype, m, n, k, opa, opb, alpha, beta):
@@ -132,3 +133,19 @@ def test_gemm_a_padding_nan_alpha0_zero_dims_host():
     b = run_gemm_a("T", "N", m, n, k, np.float32(1.5), A4, k, k * m, batch, B4, k, np.float32(0.5), C4, m, m * n,
                    host=True)
     assert mismatches(a, b) == 0
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [2, 7, 16])
+@pytest.mark.parametrize("opa", ["N", "T"])
+def test_gemm_a_square_many_tiles(dtype, n, opa):
+    """The square n <= 16 kernel over many CTA tiles (grid-stride loop, ragged last tile)."""
+    g = rng(n * 7 + (opa == "T"))
+    batch = 60_001
+    A = uniform(g, n * n * batch, dtype)
+    B = uniform(g, n * n, dtype)
+    Cm = uniform(g, n * n * batch, dtype)
+    got = run_gemm_a(opa, "T", n, n, n, dtype(-0.625), A, n, n * n, batch, B, n, dtype(0.5), Cm, n, n * n)
+    want = Cm.copy()
+    oracle().gemm_a(opa, "T", n, n, n, batch, dtype(-0.625), A, n, n * n, B, n, dtype(0.5), want, n, n * n)
+    assert mismatches(got, want) == 0

@@ -48,6 +48,35 @@ def bench(dims3, n, batch, dtype, reps=10):
           f"{ms:8.3f} ms  {flops / ms / 1e9:8.1f} TF/s  {byts / ms / 1e6:7.1f} GB/s  (min {ts[0]:.3f})", flush=True)
 
 
+def bench_gemm_a(n, dtype, opa="N", reps=10):
+    """gemm_a C^p = alpha op(A^p) B + beta C^p, square n, 2 GiB of A (device-resident)."""
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    es = 4 if dtype == "f32" else 8
+    e = n * n
+    batch = max(1, int(2 * 1024 ** 3 // (e * es)))
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A = torch.rand(e * batch, dtype=tdt, device="cuda", generator=g) * 2 - 1
+    Cm = torch.empty(e * batch, dtype=tdt, device="cuda")
+    B = torch.rand(e, dtype=tdt, device="cuda", generator=g) * 2 - 1
+    s = torch.cuda.Stream()
+    ex = kb.Exec(stream=s, asynchronous=True)
+    args = (opa, "N", n, n, n, 1.0, BatchView(MatrixView(A, n, n, n), batch, e), MatrixView(B, n, n, n), 0.0,
+            BatchView(MatrixView(Cm, n, n, n), batch, e))
+    for _ in range(3):
+        kb.gemm_a(*args, exec_=ex)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in evs:
+        a.record(s)
+        kb.gemm_a(*args, exec_=ex)
+        b.record(s)
+    torch.cuda.synchronize()
+    ts = sorted(a.elapsed_time(b) for a, b in evs)
+    ms = ts[len(ts) // 2]
+    print(f"gemm_a op{opa} {dtype} n={n:2d} batch={batch:8d} {ms:8.3f} ms  {2 * n ** 3 * batch / ms / 1e9:8.1f} TF/s  "
+          f"{2 * e * es * batch / ms / 1e6:7.1f} GB/s  (min {ts[0]:.3f})", flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "main"
     if which == "main":
@@ -60,6 +89,11 @@ if __name__ == "__main__":
     elif which == "one":  # one <2|3> <n> <f32|f64> <batch> [reps]
         reps = int(sys.argv[6]) if len(sys.argv) > 6 else 3
         bench(sys.argv[2] == "3", int(sys.argv[3]), int(sys.argv[5]), sys.argv[4], reps=reps)
+    elif which == "gemm_a":  # gemm_a [f32|f64]: square n = 1..16, op_a N and T
+        for dt in sys.argv[2:] or ["f32", "f64"]:
+            for n in range(1, 17):
+                for opa in ("N", "T"):
+                    bench_gemm_a(n, dt, opa, reps=5)
     elif which == "sweepd":  # sweepd <2|3> <f32|f64>: one rank / dtype of the size sweep
         dims3, dt = sys.argv[2] == "3", sys.argv[3]
         es = 4 if dt == "f32" else 8
