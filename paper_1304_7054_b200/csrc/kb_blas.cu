@@ -89,7 +89,18 @@ __global__ void __launch_bounds__(256) kron1_sq_kernel(const T* __restrict__ X, 
   for (long long g = (long long)blockIdx.x * 8 + warp; g < ngroups; g += (long long)gridDim.x * 8) {
     const long long first = g * 32;
     const int valid = (int)(batch - first < 32 ? batch - first : 32);
-    for (int idx = lane; idx < valid * N; idx += 32) s[(idx / N) * SE + idx % N] = X[first * N + idx];
+    if (valid == 32) {  // full group: all N loads of this lane in flight before the smem stores
+      T v[N];
+#pragma unroll
+      for (int t = 0; t < N; ++t) v[t] = __ldcs(X + first * N + lane + 32 * t);
+#pragma unroll
+      for (int t = 0; t < N; ++t) {
+        const int idx = lane + 32 * t;
+        s[(idx / N) * SE + idx % N] = v[t];
+      }
+    } else {
+      for (int idx = lane; idx < valid * N; idx += 32) s[(idx / N) * SE + idx % N] = X[first * N + idx];
+    }
     __syncwarp();
     if (lane < valid) {
       T acc[N];
@@ -117,7 +128,15 @@ __global__ void __launch_bounds__(256) kron1_sq_kernel(const T* __restrict__ X, 
       for (int i = 0; i < N; ++i) s[lane * SE + i] = acc[i];  // this lane's own slot: no cross-lane hazard
     }
     __syncwarp();
-    for (int idx = lane; idx < valid * N; idx += 32) Y[first * N + idx] = s[(idx / N) * SE + idx % N];
+    if (valid == 32) {
+#pragma unroll
+      for (int t = 0; t < N; ++t) {
+        const int idx = lane + 32 * t;
+        __stcs(Y + first * N + idx, s[(idx / N) * SE + idx % N]);
+      }
+    } else {
+      for (int idx = lane; idx < valid * N; idx += 32) Y[first * N + idx] = s[(idx / N) * SE + idx % N];
+    }
     __syncwarp();
   }
 }

@@ -77,6 +77,35 @@ def bench_gemm_a(n, dtype, opa="N", reps=10):
           f"{2 * e * es * batch / ms / 1e6:7.1f} GB/s  (min {ts[0]:.3f})", flush=True)
 
 
+def bench_kron1(n, dtype, reps=10):
+    """kron1 y^p = A x^p (shared A), square n, 2 GiB of x (device-resident)."""
+    from paper_1304_7054_b200 import VectorView
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    es = 4 if dtype == "f32" else 8
+    batch = max(1, int(2 * 1024 ** 3 // (n * es)))
+    g = torch.Generator(device="cuda").manual_seed(1)
+    X = torch.rand(n * batch, dtype=tdt, device="cuda", generator=g) * 2 - 1
+    Y = torch.empty(n * batch, dtype=tdt, device="cuda")
+    A = torch.rand(n * n, dtype=tdt, device="cuda", generator=g) * 2 - 1
+    s = torch.cuda.Stream()
+    ex = kb.Exec(stream=s, asynchronous=True)
+    args = ("N", n, n, 1.0, MatrixView(A, n, n, n), BatchView(VectorView(X, n), batch, n), 0.0,
+            BatchView(VectorView(Y, n), batch, n))
+    for _ in range(3):
+        kb.kron1(*args, exec_=ex)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in evs:
+        a.record(s)
+        kb.kron1(*args, exec_=ex)
+        b.record(s)
+    torch.cuda.synchronize()
+    ts = sorted(a.elapsed_time(b) for a, b in evs)
+    ms = ts[len(ts) // 2]
+    print(f"kron1 {dtype} n={n:2d} batch={batch:9d} {ms:8.3f} ms  {2 * n * n * batch / ms / 1e9:8.1f} TF/s  "
+          f"{2 * n * es * batch / ms / 1e6:7.1f} GB/s  (min {ts[0]:.3f})", flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "main"
     if which == "main":
@@ -94,6 +123,10 @@ if __name__ == "__main__":
             for n in range(1, 17):
                 for opa in ("N", "T"):
                     bench_gemm_a(n, dt, opa, reps=5)
+    elif which == "kron1":  # kron1 [f32|f64]: square n = 1..16
+        for dt in sys.argv[2:] or ["f32", "f64"]:
+            for n in range(1, 17):
+                bench_kron1(n, dt, reps=5)
     elif which == "sweepd":  # sweepd <2|3> <f32|f64>: one rank / dtype of the size sweep
         dims3, dt = sys.argv[2] == "3", sys.argv[3]
         es = 4 if dt == "f32" else 8
