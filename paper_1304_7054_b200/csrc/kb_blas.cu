@@ -18,6 +18,8 @@
 // the per-entry operand reads broadcast through L1 and the output writes are
 // coalesced; the shared matrix is read through the read-only path (it stays
 // in L1/L2). Any shape, op and stride; identical arithmetic to the CPU path.
+#include <cstdlib>
+
 #include "kb_kernels.h"
 
 namespace kb {
@@ -305,11 +307,122 @@ __global__ void __launch_bounds__(256) gemm_a_sq_kernel(const T* __restrict__ A,
   if constexpr (G::PIPE) cp_async_wait<0>();
 }
 
+// Warp-granular variant (the default for most sizes): each warp owns WE = 32/n entries (lane -> entry
+// lane/n, column lane%n) in a private smem slice; no CTA barrier after the
+// one-time w fill, so warps drift freely and hide each other's load latency.
+template <typename T, int N>
+struct GaWarp {
+  static constexpr int CS = GaTile<T, N>::CS, EST = GaTile<T, N>::EST;
+  static constexpr int WE = 32 / N;             // entries per warp group
+  static constexpr int LPT = (WE * N * N + 31) / 32;  // loads per lane per group
+  static constexpr int WARPS = 8;
+};
+
+template <typename T, int N, bool OPT>
+__global__ void __launch_bounds__(256) gemm_a_sqw_kernel(const T* __restrict__ A, T* __restrict__ Cm, long long batch,
+                                                         T alpha, int beta_mode, T beta,
+                                                         const __grid_constant__ GaConsts<T, N> gc) {
+  using G = GaWarp<T, N>;
+  constexpr int NN = N * N, CS = G::CS, EST = G::EST, WE = G::WE, LPT = G::LPT;
+  __shared__ __align__(16) T sa_all[G::WARPS * WE * EST];
+  __shared__ T sw[NN];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < NN; i += 256) sw[(i % N) * N + i / N] = gc.w[i];  // sw[kk*N + c]
+  __syncthreads();
+  T* sa = sa_all + warp * WE * EST;
+  const int el = lane / N, c = lane % N;
+  const long long ngroups = (batch + WE - 1) / WE;
+  for (long long grp = (long long)blockIdx.x * G::WARPS + warp; grp < ngroups; grp += (long long)gridDim.x * G::WARPS) {
+    const long long first = grp * WE;
+    const int valid = (int)(batch - first < WE ? batch - first : WE);
+    const int lim = valid * NN;
+    const T* src = A + first * NN;
+    {
+      T v[LPT];
+#pragma unroll
+      for (int t = 0; t < LPT; ++t)
+        if (lane + 32 * t < lim) v[t] = __ldcs(src + lane + 32 * t);
+#pragma unroll
+      for (int t = 0; t < LPT; ++t) {
+        const int g = lane + 32 * t;
+        if (g < lim) {
+          const int e = g / NN, r = g - e * NN;
+          const int i = OPT ? r / N : r % N, kk = OPT ? r % N : r / N;
+          sa[e * EST + i + kk * CS] = v[t];
+        }
+      }
+    }
+    __syncwarp();
+    T acc[N];
+    const bool act = el < valid;
+    T* cg = Cm + (first + el) * NN + c * N;
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = OPT || beta_mode == kBetaZero ? T(0) : beta_init(beta_mode, beta, cg[i]);
+      const T* ae = sa + el * EST;
+#pragma unroll
+      for (int kk = 0; kk < N; ++kk) {
+        const T w = sw[kk * N + c];
+        const T* col = ae + kk * CS;
+        if constexpr (sizeof(T) == 4) {
+          float a[(N + 3) / 4 * 4];
+#pragma unroll
+          for (int i = 0; i < N; i += 4) *reinterpret_cast<float4*>(a + i) = *reinterpret_cast<const float4*>(col + i);
+#pragma unroll
+          for (int i = 0; i + 1 < N; i += 2) {
+            const float2 d = ffma2_s(make_float2(a[i], a[i + 1]), w, make_float2(acc[i], acc[i + 1]));
+            acc[i] = d.x;
+            acc[i + 1] = d.y;
+          }
+          if constexpr (N % 2) acc[N - 1] = fma_rn(a[N - 1], w, acc[N - 1]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < N; ++i) acc[i] = fma_rn(col[i], w, acc[i]);
+        }
+      }
+      if constexpr (OPT) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const T init = beta_mode == kBetaZero ? T(0) : mul_rn(beta, cg[i]);
+          acc[i] = fma_rn(alpha, acc[i], init);
+        }
+      }
+    }
+    __syncwarp();  // the warp is done reading op(A) out of its slice
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) sa[el * EST + i + c * CS] = acc[i];
+    }
+    __syncwarp();
+    T* dst = Cm + first * NN;
+#pragma unroll
+    for (int t = 0; t < LPT; ++t) {
+      const int g = lane + 32 * t;
+      if (g < lim) __stcs(dst + g, sa[(g / NN) * EST + (g % NN) % N + ((g % NN) / N) * CS]);
+    }
+    __syncwarp();
+  }
+}
+
 template <typename T, int N>
 static cudaError_t launch_gemm_a_sq_n(bool opt, const T* hw, const T* A, T* Cm, long long batch, T alpha,
                                       int beta_mode, T beta, int sm_count, cudaStream_t s) {
   GaConsts<T, N> gc;
   for (int i = 0; i < N * N; ++i) gc.w[i] = hw[i];
+  // warp-granular kernel by default; the CTA-tile kernel where it measured
+  // faster (fp64 n = 12-15, profiles/r01_gemm_a_square.txt). KB_GA_WARP=0/1 forces one.
+  static const int wv = [] { const char* e = std::getenv("KB_GA_WARP"); return e ? std::atoi(e) : -1; }();
+  constexpr bool warp_default = !(sizeof(T) == 8 && N >= 12 && N <= 15);
+  if (wv == 1 || (wv < 0 && warp_default)) {
+    auto kw = opt ? gemm_a_sqw_kernel<T, N, true> : gemm_a_sqw_kernel<T, N, false>;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kw, 256, 0) != cudaSuccess || occ < 1) occ = 1;
+    const long long ng = (batch + GaWarp<T, N>::WE - 1) / GaWarp<T, N>::WE;
+    const long long want = (ng + 7) / 8, cap = (long long)sm_count * occ;
+    const int grid = (int)(want < cap ? want : cap);
+    kw<<<grid > 0 ? grid : 1, 256, 0, s>>>(A, Cm, batch, alpha, beta_mode, beta, gc);
+    return cudaGetLastError();
+  }
   const long long ntiles = (batch + GaTile<T, N>::E - 1) / GaTile<T, N>::E;
   auto kern = opt ? gemm_a_sq_kernel<T, N, true> : gemm_a_sq_kernel<T, N, false>;
   using G = GaTile<T, N>;

@@ -19,3 +19,13 @@ def test_kernel_switches_bitwise(env):
     r = subprocess.run([sys.executable, os.path.join(HERE, "variant_check.py")], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("warp", ["0", "1"])
+def test_gemm_a_square_kernels_both(warp):
+    """Both square gemm_a kernels (CTA tile / warp-granular, KB_GA_WARP) stay bit-exact vs the oracle."""
+    env = dict(os.environ, KB_GA_WARP=warp)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+                        os.path.join(HERE, "test_gpu_blas.py"), "-k", "gemm_a"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
