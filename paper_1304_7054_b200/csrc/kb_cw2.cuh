@@ -24,6 +24,16 @@
 
 namespace kb {
 
+// 2-D column-wise constants: A_r columns at an even stride, so every row pair
+// {i, i+1} (i even) is an 8-byte-aligned constant-bank pair (one UR.F32x2
+// FFMA2 operand, no UMOVs at odd n); w as in SqConsts2.
+template <typename T, int N>
+struct SqConstsCw2 {
+  static constexpr int LD = N % 2 ? N + 1 : N;
+  T a[N * LD];  // a[l*LD + i] = A_r(i, l)
+  T w[N * N];   // w[j*N + m] = fl(alpha B_r(j, m))
+};
+
 template <typename T, int N>
 struct Cw2 {
   static constexpr int ES = sizeof(T);
@@ -86,7 +96,7 @@ struct Cw2 {
 
 template <typename T, int N, bool YS>
 __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
-    kron2_cw_kernel(const Kron2Params<T> p, const __grid_constant__ SqConsts2<T, N> kc, const long long ngroups) {
+    kron2_cw_kernel(const Kron2Params<T> p, const __grid_constant__ SqConstsCw2<T, N> kc, const long long ngroups) {
   constexpr bool ystage = YS;  // compile-time: the other store path is not even in the binary
   using K = Cw2<T, N>;
   constexpr int R = K::R, TPI = K::TPI, EPW = K::EPW, NN = K::NN, S = K::STAGES, SLOT = K::SLOT;
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
 #pragma unroll
         for (int ll = 0; ll < K::VXR; ++ll)
 #pragma unroll
-          for (int k = 0; k < K::CA; ++k) axpy_pairs_c(acc[k], kc.a + (l0 + ll) * N, x[k][ll], N);
+          for (int k = 0; k < K::CA; ++k) axpy_pairs_c(acc[k], kc.a + (l0 + ll) * kc.LD, x[k][ll], N);
       }
 #pragma unroll
       for (int k = 0; k < K::CA; ++k)

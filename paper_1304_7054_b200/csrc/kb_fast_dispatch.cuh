@@ -120,11 +120,10 @@ static cudaError_t launch2cw(const Kron2Params<T>& p, const T* ha, const T* hw, 
   const long long ngroups = (p.batch + K::EPW - 1) / K::EPW;
   const long long want = (ngroups + K::WARPS - 1) / K::WARPS;
   const int grid = (int)(want < (long long)sm_count * occ ? want : (long long)sm_count * occ);
-  SqConsts2<T, N> kc;
-  for (int i = 0; i < N * N; ++i) {
-    kc.a[i] = ha[i];
-    kc.w[i] = hw[i];
-  }
+  SqConstsCw2<T, N> kc;
+  for (int l = 0; l < N; ++l)
+    for (int i = 0; i < N; ++i) kc.a[l * kc.LD + i] = ha[l * N + i];
+  for (int i = 0; i < N * N; ++i) kc.w[i] = hw[i];
   kern<<<grid, threads, smem, s>>>(p, kc, ngroups);
   return cudaGetLastError();
 }
