@@ -12,13 +12,13 @@ endif
 PKG       := paper_1304_7054_b200
 CSRC      := $(PKG)/csrc
 OBJDIR    := build/obj
-SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast_switch.cu $(CSRC)/kb_tc.cu $(CSRC)/kb_blas.cu \
+SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_devmgr.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast_switch.cu $(CSRC)/kb_tc.cu $(CSRC)/kb_blas.cu \
              $(sort $(wildcard $(CSRC)/kb_sz*.cu))
 OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 HDRS      := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/kronbatch_b200.h
 LIB       := $(PKG)/libkronbatch_b200.so
 
-.PHONY: all lib oracle cpptest kronbench clean
+.PHONY: all lib oracle cpptest kronbench sanitize clean
 all: lib oracle
 
 lib: $(LIB)
@@ -39,6 +39,13 @@ cpptest: $(CPPTESTS)
 build/cpptest/test_dropin: tests/cpp/test_dropin.cpp $(LIB) $(wildcard include/kronbatch/*.hpp)
 	@mkdir -p build/cpptest
 	$(CXX_HOST) -O2 -std=gnu++20 -Iinclude -o $@ $< -L$(PKG) -lkronbatch_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
+# compute-sanitizer driver: one small call of every kernel family through the C ABI
+sanitize: build/sanitize/kb_sanitize
+build/sanitize/kb_sanitize: tools/sanitize/kb_sanitize.cpp $(LIB) include/kronbatch_b200.h
+	@mkdir -p build/sanitize
+	$(CXX_HOST) -O2 -std=gnu++17 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -lkronbatch_b200 \
+	  -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
 
 # native bench CLI (the reference's `bench` flags + CSV schema, on the B200 library)
 kronbench: tools/kronbench/kronbench

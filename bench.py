@@ -2,26 +2,39 @@
 """bench.py -- the driver's benchmark contract for kronbatch-b200.
 
 Headline workload (BASELINE.json configs[1]): batched 2-D Kronecker action,
-fp32, n = 16, batch 4,194,304 entries PER GPU (weak scaling: every rank owns an
-independent contiguous shard, no data-path collective). One "step" = one pass
-of kron2 over the rank's batch.
+fp32, n = 16, 4,194,304 entries PER GPU (weak scaling: every GPU owns an
+independent contiguous part, no data-path collective). One "step" = one pass
+of kron2 over the batch.
 
-  value  : GFlop/s (paper flop count 4 n^3 per entry) over the whole job, inputs
-           resident in HBM, device-timed with CUDA events on the launching
-           stream, max over ranks.
-  e2e    : same metric through the public API with PINNED HOST buffers
-           (host->device copy of X and device->host copy of Y inside every
-           step; the library pipelines the staging in chunks).
-  roofline, cpu_baseline, clocks, gpu_launches: see DESIGN.md "Measurement".
-  extra  : the other BASELINE configs (3-D fp32 n=16 / n=10, 3-D fp64 n=16,
-           2-D fp32 n=10) measured the same way, for the record.
+  value  : GFlop/s (paper flop count 4 n^3 per entry) over the whole job,
+           inputs resident in HBM, device-timed with CUDA events on the
+           launching stream(s), max over GPUs.
+  e2e    : same metric through the public API with PINNED HOST buffers (X
+           host->device and Y device->host inside every step; the library
+           pipelines the staging in chunks). `e2e_pageable`: the same with
+           ordinary pageable numpy buffers (pinned bounce buffers + copy pool).
+  roofline, cpu_baseline, parity, clocks, gpu_launches: DESIGN.md §5.
+  extra  : the other BASELINE configs, measured the same way: 3-D fp32 n=16 /
+           n=10 (262,144 per GPU, weak), 3-D fp64 n=16 (131,072 TOTAL split over
+           the GPUs: configs[3] is a strong-scaling config), 2-D fp32 n=10
+           (65,536 per GPU; 52 MB < L2, so timed over rotating buffer sets
+           that exceed 2x L2, eagerly and as a CUDA-graph replay).
+
+Multi-GPU:
+  torchrun --nproc-per-node N bench.py --gpus N   one process per GPU (the
+      driver's launch); host barrier + max-over-ranks through a gloo group
+      (CPU), no NCCL anywhere.
+  python bench.py --gpus N                          one process driving N GPUs
+      through the library's own multi-device entry points (kb.kron2_parts for
+      device-resident parts, kb.Exec(devices=...) sharding for host buffers).
+      Refuses if fewer than N GPUs are visible, unless --devices lists the
+      ordinals explicitly (e.g. --devices 0,0 on a 1-GPU box); n_gpus always
+      reports the number of DISTINCT GPUs that ran.
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/libkronref.so = the unmodified kronbatch::kron2<float> compiled
-from /root/reference, OpenMP over all host cores) on a bounded sample.
-
-Run:  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-      torchrun --nproc-per-node N bench.py --gpus N ...
+from /root/reference, OpenMP over all host cores, pinned) on the FULL headline
+config, one step = one full pass.
 """
 from __future__ import annotations
 
@@ -39,18 +52,18 @@ sys.path.insert(0, ROOT)
 
 METRIC = "batched Kron GFlop/s + HBM GB/s (n=16 fp32 2-D & 3-D) at 1/2/4/8 B200"
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
-FP32_PEAK_TFLOPS = 72.5    # measured FFMA peak (tools/microbench/fma_tput.cu, profiles/)
+FP32_PEAK_TFLOPS = 72.5    # measured FFMA peak (tools/microbench/fma_tput.cu, profiles/r01_fma_tput.txt)
 FP64_PEAK_TFLOPS = 33.6    # measured DFMA peak
 FFMA2_PEAK_TFLOPS = 67.1   # measured fma.rn.f32x2 (FFMA2) peak -- the instruction the fp32 kernels issue
                            # (profiles/r01_fma_tput.txt); reported beside, never as, the roofline
 
 WORKLOADS = {
-    # name: (dims3, n, dtype, batch per GPU)
-    "kron2-f32-n16": (False, 16, "f32", 4194304),
-    "kron3-f32-n16": (True, 16, "f32", 262144),
-    "kron3-f32-n10": (True, 10, "f32", 262144),
-    "kron3-f64-n16": (True, 16, "f64", 131072),
-    "kron2-f32-n10": (False, 10, "f32", 65536),
+    # name: (dims3, n, dtype, batch, scaling) -- weak: batch per GPU; strong: total batch split over GPUs
+    "kron2-f32-n16": (False, 16, "f32", 4194304, "weak"),
+    "kron3-f32-n16": (True, 16, "f32", 262144, "weak"),
+    "kron3-f32-n10": (True, 10, "f32", 262144, "weak"),
+    "kron3-f64-n16": (True, 16, "f64", 131072, "strong"),
+    "kron2-f32-n10": (False, 10, "f32", 65536, "weak"),
 }
 HEADLINE = "kron2-f32-n16"
 
@@ -94,8 +107,8 @@ class ClockSampler:
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index, period_s=0.002):
-        self.index, self.period = index, period_s
+    def __init__(self, indices, period_s=0.002):
+        self.indices, self.period = sorted(set(indices)), period_s
         self.sm, self.reasons, self.smax = [], set(), None
         self._stop = threading.Event()
 
@@ -105,8 +118,8 @@ class ClockSampler:
 
             nv.nvmlInit()
             self.nv = nv
-            self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
-            self.smax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.hs = [nv.nvmlDeviceGetHandleByIndex(i) for i in self.indices]
+            self.smax = nv.nvmlDeviceGetMaxClockInfo(self.hs[0], nv.NVML_CLOCK_SM)
             self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
         except Exception:
@@ -116,14 +129,15 @@ class ClockSampler:
     def _run(self):
         nv = self.nv
         while not self._stop.is_set():
-            try:
-                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit:
-                        self.reasons.add(name)
-            except Exception:
-                pass
+            for h in self.hs:
+                try:
+                    self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for bit, name in self.REASONS.items():
+                        if r & bit:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
             time.sleep(self.period)
 
     def __exit__(self, *exc):
@@ -136,179 +150,337 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
-# --------------------------------------------------------------- our arm --
+# ------------------------------------------------------------- the topology --
 
-def make_problem(kb, torch, dims3, n, dtype, batch, device, host=False, seed=1):
-    tdt = torch.float32 if dtype == "f32" else torch.float64
-    e = n ** (3 if dims3 else 2)
-    g = torch.Generator(device=device).manual_seed(seed)
-    mk = lambda cnt: (torch.rand(cnt, dtype=tdt, device=device, generator=g) * 2 - 1)
-    # The constant matrices are small host arrays, as in the reference API: the
-    # library folds them into kernel parameters (no per-call device->host sync).
-    A, B, Cm = (mk(n * n).cpu() for _ in range(3))
-    X = mk(e * batch)
-    Y = torch.empty(e * batch, dtype=tdt, device=device)
-    if host:
-        X = X.cpu().pin_memory()
-        Y = torch.empty(e * batch, dtype=tdt).pin_memory()
-    MV, BV = kb.MatrixView, kb.BatchView
-    if dims3:
-        pr = kb.KronProblem3D(m_a=n, n_a=n, m_b=n, n_b=n, m_c=n, n_c=n)
-        args = (pr, MV(A, n, n, n), MV(B, n, n, n), MV(Cm, n, n, n),
-                BV(kb.Array3View(X, n, n, n, n, n * n), batch, e), BV(kb.Array3View(Y, n, n, n, n, n * n), batch, e),
-                kb.Workspace(None, n * n * n * batch))
-        return kb.kron3, args, (X, Y)
-    pr = kb.KronProblem2D(m_a=n, n_a=n, m_b=n, n_b=n)
-    args = (pr, MV(A, n, n, n), MV(B, n, n, n), BV(MV(X, n, n, n), batch, e), BV(MV(Y, n, n, n), batch, e))
-    return kb.kron2, args, (X, Y)
+class Topo:
+    """Where this process runs: `devices` it drives (one per part) and the
+    torchrun world it belongs to (gloo group for the host barrier / max)."""
 
+    def __init__(self, devices, world, rank):
+        self.devices, self.world, self.rank = list(devices), world, rank
 
-def dist_max(torch, v, world):
-    if world <= 1:
-        return v
-    import torch.distributed as dist
+    @property
+    def parts(self):
+        return len(self.devices)
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    @property
+    def n_gpus(self):
+        return len(set(self.devices)) * self.world
 
+    @property
+    def total_parts(self):
+        return self.parts * self.world
 
-def barrier(world):
-    if world > 1:
+    def part_index(self, i):
+        return self.rank * self.parts + i
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    def max(self, v):
+        return self._reduce(v, "MAX")
+
+    def sum(self, v):
+        return self._reduce(v, "SUM")
+
+    def _reduce(self, v, op):
+        if self.world <= 1:
+            return v
+        import torch
         import torch.distributed as dist
 
-        dist.barrier()
+        t = torch.tensor([float(v)], dtype=torch.float64)
+        dist.all_reduce(t, op=getattr(dist.ReduceOp, op))
+        return float(t.item())
 
 
-def time_device(kb, torch, name, steps, warmup, world, rank):
-    """Device-resident timing: K launches on our stream between events; returns
-    (ms per step (max over ranks), per-launch mean ms, launches)."""
-    dims3, n, dtype, batch = WORKLOADS[name]
-    fn, args, keep = make_problem(kb, torch, dims3, n, dtype, batch, "cuda")
-    stream = torch.cuda.Stream()
-    ex = kb.Exec(stream=stream, asynchronous=True)
-    for _ in range(max(warmup, 3)):
-        fn(*args, exec_=ex)
-    torch.cuda.synchronize()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
-    barrier(world)
-    torch.cuda.synchronize()
+def part_batch(topo, scaling, batch, i):
+    """Entries of part i of this process: weak -> `batch` per part; strong ->
+    the contiguous slice of `batch` total (paper_1304_7054_b200.shard)."""
+    if scaling == "weak":
+        return batch
+    from paper_1304_7054_b200.shard import shard_range
+
+    p0, p1 = shard_range(topo.part_index(i), topo.total_parts, batch)
+    return p1 - p0
+
+
+# --------------------------------------------------------------- our arm --
+
+def make_consts(torch, n, dtype, seed=1):
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    g = torch.Generator().manual_seed(seed)
+    # host arrays, as in the reference API: the library folds them into kernel parameters
+    return [(torch.rand(n * n, dtype=tdt, generator=g) * 2 - 1) for _ in range(3)]
+
+
+def views(kb, dims3, n, X, Y, batch):
+    e = n ** (3 if dims3 else 2)
+    if dims3:
+        return (kb.BatchView(kb.Array3View(X, n, n, n, n, n * n), batch, e),
+                kb.BatchView(kb.Array3View(Y, n, n, n, n, n * n), batch, e))
+    return kb.BatchView(kb.MatrixView(X, n, n, n), batch, e), kb.BatchView(kb.MatrixView(Y, n, n, n), batch, e)
+
+
+def problem(kb, dims3, n):
+    if dims3:
+        return kb.KronProblem3D(m_a=n, n_a=n, m_b=n, n_b=n, m_c=n, n_c=n)
+    return kb.KronProblem2D(m_a=n, n_a=n, m_b=n, n_b=n)
+
+
+class DeviceWorkload:
+    """Device-resident buffers of one workload on every device of this
+    process (`sets` rotating X/Y sets per part), and a step function that runs
+    one pass over them: kron2/kron3 for one part, kron{2,3}_parts for several
+    (the library's multi-device entry point), asynchronously on one stream per
+    part so the caller brackets each step with CUDA events."""
+
+    def __init__(self, kb, torch, topo, name, sets=1):
+        self.kb, self.torch, self.topo = kb, torch, topo
+        dims3, n, dtype, batch, scaling = WORKLOADS[name]
+        self.dims3, self.n, self.name = dims3, n, name
+        self.batches = [part_batch(topo, scaling, batch, i) for i in range(topo.parts)]
+        tdt = torch.float32 if dtype == "f32" else torch.float64
+        e = n ** (3 if dims3 else 2)
+        self.A, self.B, self.C = make_consts(torch, n, dtype)
+        self.streams = [torch.cuda.Stream(device=d) for d in topo.devices]
+        self.bufs = []  # [set][part] -> (X, Y)
+        for s in range(sets):
+            row = []
+            for i, d in enumerate(topo.devices):
+                g = torch.Generator(device=f"cuda:{d}").manual_seed(1 + 7919 * s + i)
+                X = torch.rand(e * max(1, self.batches[i]), dtype=tdt, device=f"cuda:{d}", generator=g) * 2 - 1
+                Y = torch.empty(e * max(1, self.batches[i]), dtype=tdt, device=f"cuda:{d}")
+                row.append((X, Y))
+            self.bufs.append(row)
+        for d in set(topo.devices):
+            torch.cuda.synchronize(d)
+        MV = kb.MatrixView
+        self.mA, self.mB, self.mC = MV(self.A, n, n, n), MV(self.B, n, n, n), MV(self.C, n, n, n)
+        self.pr = problem(kb, dims3, n)
+        self.execs = [kb.Exec(stream=s, asynchronous=True) for s in self.streams]
+
+    def step(self, k=0):
+        kb, row = self.kb, self.bufs[k % len(self.bufs)]
+        if self.topo.parts == 1:
+            (X, Y), b = row[0], self.batches[0]
+            xv, yv = views(kb, self.dims3, self.n, X, Y, b)
+            if self.dims3:
+                kb.kron3(self.pr, self.mA, self.mB, self.mC, xv, yv, kb.Workspace(None, self.n ** 3 * b),
+                         exec_=self.execs[0])
+            else:
+                kb.kron2(self.pr, self.mA, self.mB, xv, yv, exec_=self.execs[0])
+            return
+        parts = []
+        for i, d in enumerate(self.topo.devices):
+            xv, yv = views(kb, self.dims3, self.n, row[i][0], row[i][1], self.batches[i])
+            parts.append(kb.Part(d, xv, yv, self.streams[i]))
+        if self.dims3:
+            kb.kron3_parts(self.pr, self.mA, self.mB, self.mC, parts, asynchronous=True)
+        else:
+            kb.kron2_parts(self.pr, self.mA, self.mB, parts, asynchronous=True)
+
+    def entries(self):
+        return sum(self.batches)
+
+    def sync(self):
+        for d in set(self.topo.devices):
+            self.torch.cuda.synchronize(d)
+
+
+def time_device(kb, torch, topo, name, steps, warmup, sets=1):
+    """Device-resident timing: `steps` passes, each bracketed by CUDA events
+    on every part's stream; returns (ms per step = max over parts and ranks,
+    mean per-launch ms of part 0, our kernel launches, kernel path, entries
+    this process ran per step)."""
+    w = DeviceWorkload(kb, torch, topo, name, sets)
+    for k in range(max(warmup, 3)):
+        w.step(k)
+    w.sync()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+          for _ in w.streams]
+    t0 = [torch.cuda.Event(enable_timing=True) for _ in w.streams]
+    t1 = [torch.cuda.Event(enable_timing=True) for _ in w.streams]
+    topo.barrier()
+    w.sync()
     l0 = kb.launch_count()
-    t_all0 = torch.cuda.Event(enable_timing=True)
-    t_all1 = torch.cuda.Event(enable_timing=True)
-    t_all0.record(stream)
-    for i in range(steps):
-        starts[i].record(stream)
-        fn(*args, exec_=ex)
-        ends[i].record(stream)
-    t_all1.record(stream)
-    torch.cuda.synchronize()
+    for s, e in zip(w.streams, t0):
+        e.record(s)
+    for k in range(steps):
+        for i, s in enumerate(w.streams):
+            ev[i][k][0].record(s)
+        w.step(k)
+        for i, s in enumerate(w.streams):
+            ev[i][k][1].record(s)
+    for s, e in zip(w.streams, t1):
+        e.record(s)
+    w.sync()
     launches = kb.launch_count() - l0
-    barrier(world)
-    total_ms = t_all0.elapsed_time(t_all1)
-    per_launch = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = dist_max(torch, total_ms, world)
-    del keep
-    return total_ms / steps, statistics.mean(per_launch), launches, kb.last_path()
+    topo.barrier()
+    total_ms = max(a.elapsed_time(b) for a, b in zip(t0, t1))
+    per_launch = statistics.mean(a.elapsed_time(b) for a, b in ev[0])
+    total_ms = topo.max(total_ms)
+    path = kb.last_path()
+    entries = w.entries()
+    del w
+    return total_ms / steps, per_launch, launches, path, entries
 
 
-def time_graph(kb, torch, name, steps, world):
-    """Launch-overhead-free device time: `steps` calls captured into one CUDA
-    graph (the library's kernel launches are capturable on the exec stream),
-    replayed between events; returns ms per launch (max over ranks)."""
-    dims3, n, dtype, batch = WORKLOADS[name]
-    fn, args, keep = make_problem(kb, torch, dims3, n, dtype, batch, "cuda")
-    stream = torch.cuda.Stream()
-    ex = kb.Exec(stream=stream, asynchronous=True)
-    for _ in range(3):
-        fn(*args, exec_=ex)
-    torch.cuda.synchronize()
+def time_graph(kb, torch, topo, name, steps, sets):
+    """Launch-overhead-free device time (single part): `steps` calls over the
+    rotating buffer sets captured into one CUDA graph (the library's launches
+    are capturable on the exec stream), replayed between events; ms per launch."""
+    w = DeviceWorkload(kb, torch, topo, name, sets)
+    for k in range(3):
+        w.step(k)
+    w.sync()
+    stream = w.streams[0]
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
-        for _ in range(steps):
-            fn(*args, exec_=ex)
+        for k in range(steps):
+            w.step(k)
     for _ in range(2):
         g.replay()
-    torch.cuda.synchronize()
+    w.sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier(world)
+    topo.barrier()
     with torch.cuda.stream(stream):
         e0.record(stream)
         g.replay()
         e1.record(stream)
-    torch.cuda.synchronize()
-    ms = dist_max(torch, e0.elapsed_time(e1) / steps, world)
-    del keep, g
+    w.sync()
+    ms = topo.max(e0.elapsed_time(e1) / steps)
+    del w, g
     return ms
 
 
-def time_e2e(kb, torch, name, steps, warmup, world):
-    """End to end through the public API with pinned host X / Y: H2D of X and
-    D2H of Y inside every step (wall time around the synchronous call, which
-    returns only after Y is back in host memory), max over ranks."""
-    dims3, n, dtype, batch = WORKLOADS[name]
-    fn, args, (X, Y) = make_problem(kb, torch, dims3, n, dtype, batch, "cuda", host=True)
-    for _ in range(max(1, min(warmup, 2))):
-        fn(*args)
-    barrier(world)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        fn(*args)
-    dt = time.perf_counter() - t0
-    dt = dist_max(torch, dt, world)
-    return dt * 1e3 / steps, X.numel() * X.element_size(), Y.numel() * Y.element_size()
-
-
-def cpu_reference_sample(name, seconds_budget=8.0, threads=None):
-    """The reference CPU path (oracle/_ref: unmodified kronbatch::kron2/kron3
-    with OpenMP) on a bounded sample of the workload; median of reps after a
-    verified-by-the-tests warm-up. Returns (GFlop/s, cores, sample text)."""
+def time_e2e(kb, torch, topo, name, steps, warmup, pageable=False):
+    """End to end through the public API with HOST X / Y (pinned torch tensors,
+    or pageable numpy arrays): the H2D of X and the D2H of Y are inside every
+    step (wall time around the synchronous call, which returns only after Y is
+    back in host memory); several devices of this process -> one call sharded
+    by the library over kb.Exec(devices). Max over ranks."""
     import numpy as np
 
-    from oracle.oracle import Reference
-
-    dims3, n, dtype, _ = WORKLOADS[name]
-    ref = Reference()
-    if threads:
-        ref.set_threads(threads)
-    cores = ref.max_threads
-    dt = np.float32 if dtype == "f32" else np.float64
+    dims3, n, dtype, batch, scaling = WORKLOADS[name]
     e = n ** (3 if dims3 else 2)
-    sample = max(1, int((256 << 20) // (e * dt().itemsize)))  # ~256 MiB of X per rep
-    a, b, c, x, y = ref.generate_batch(dt, 1, n, dims3, sample)
-    work = np.empty(n * n * n * sample if dims3 else 0, dt)
+    total = sum(part_batch(topo, scaling, batch, i) for i in range(topo.parts))
+    npdt = np.float32 if dtype == "f32" else np.float64
+    gen = np.random.default_rng(topo.rank)
+    if pageable:
+        X = (gen.random(e * total, dtype=np.float64 if dtype == "f64" else np.float32) * 2 - 1).astype(npdt, copy=False)
+        Y = np.zeros(e * total, npdt)  # touched, like a std::vector
+    else:
+        tdt = torch.float32 if dtype == "f32" else torch.float64
+        X = (torch.rand(e * total, dtype=tdt) * 2 - 1).pin_memory()
+        Y = torch.zeros(e * total, dtype=tdt).pin_memory()
+    A, B, C = make_consts(torch, n, dtype)
+    MV = kb.MatrixView
+    xv, yv = views(kb, dims3, n, X, Y, total)
+    ex = kb.Exec(devices=topo.devices) if topo.parts > 1 else None
+    pr = problem(kb, dims3, n)
 
-    def run():
+    def call():
         if dims3:
-            ref.kron3("N", "N", "N", n, n, n, n, n, n, sample, dt(1), a, (n, n), n, b, (n, n), n, c, (n, n), n, x,
-                      (n, n, n), n, n * n, e, dt(0), y, (n, n, n), n, n * n, e, work)
+            kb.kron3(pr, MV(A, n, n, n), MV(B, n, n, n), MV(C, n, n, n), xv, yv, kb.Workspace(None, e * total),
+                     exec_=ex)
         else:
-            ref.kron2("N", "N", "N", n, n, n, n, sample, dt(1), a, (n, n), n, b, (n, n), n, x, (n, n), n, e, dt(0), y,
-                      (n, n), n, e)
+            kb.kron2(pr, MV(A, n, n, n), MV(B, n, n, n), xv, yv, exec_=ex)
 
-    run()  # warm-up (first touch, thread pool)
-    times = []
-    t_end = time.perf_counter() + seconds_budget
-    while len(times) < 3 or (time.perf_counter() < t_end and len(times) < 50):
-        t0 = time.perf_counter()
-        run()
-        times.append(time.perf_counter() - t0)
-    med = statistics.median(times)
-    gf = flops_per_entry(dims3, n) * sample / med / 1e9
-    return gf, cores, f"{sample} entries of {name} (generate_batch seed 1), median of {len(times)} reps", med
+    for _ in range(max(1, min(warmup, 2))):
+        call()
+    topo.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    dt = time.perf_counter() - t0
+    dt = topo.max(dt)
+    nbytes = e * total * (4 if dtype == "f32" else 8)
+    return dt * 1e3 / steps, nbytes, nbytes
+
+
+def cpu_reference(name, reps=10, parity=False, timeout=900):
+    """The cpu_baseline leg: oracle/cpu_ref.py in its own process (pinned
+    OpenMP, full config, median of reps; with parity, the product on the same
+    generate_batch inputs compared over the whole batch)."""
+    cmd = [sys.executable, "-m", "oracle.cpu_ref", "--workload", name, "--reps", str(reps)]
+    if parity:
+        cmd.append("--parity")
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    if r.returncode != 0:
+        raise RuntimeError(f"cpu_ref failed ({r.returncode}): {r.stderr.strip()[-400:]}")
+    return json.loads(r.stdout.strip().splitlines()[-1])
 
 
 # ------------------------------------------------------------------ main --
 
+def reference_arm(args, rank):
+    """--impl reference: the unmodified reference CPU path on the full headline
+    config, K timed steps after W warm-ups (rank 0 only)."""
+    if rank != 0:
+        return 0
+    from oracle.cpu_ref import OMP_ENV
+
+    for k, v in OMP_ENV.items():
+        os.environ.setdefault(k, v)
+    import numpy as np
+
+    from oracle.cpu_ref import host_info
+    from oracle.oracle import Reference
+
+    dims3, n, dtype, batch, _ = WORKLOADS[HEADLINE]
+    ref = Reference()
+    dt = np.float32
+    e = n * n
+    a, b, _, x, y = ref.generate_batch(dt, 1, n, dims3, batch)
+    y = np.zeros_like(x)
+
+    def run():
+        ref.kron2("N", "N", "N", n, n, n, n, batch, dt(1), a, (n, n), n, b, (n, n), n, x, (n, n), n, e, dt(0), y,
+                  (n, n), n, e)
+
+    for _ in range(args.warmup):
+        run()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    gf = flops_per_entry(dims3, n) * batch * args.steps / total / 1e9
+    cores = ref.max_threads
+    sample = (f"full config: {batch} entries per step (generate_batch seed 1), {args.steps} steps after "
+              f"{args.warmup} warm-ups, OpenMP {cores} threads pinned ({', '.join(f'{k}={v}' for k, v in OMP_ENV.items())})")
+    line = {"metric": METRIC, "value": round(gf, 3), "unit": "GFlop/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generate_batch, seed 1)",
+            "impl": "reference",
+            "config": {"workload": f"{HEADLINE}: 2-D Kronecker action fp32 n=16, batch {batch} (BASELINE configs[1]), "
+                                   "reference CPU path (oracle/_ref, unmodified kronbatch::kron2<float>)",
+                       "batch_per_gpu": batch, "same_config": True},
+            "cpu_baseline": {"value": round(gf, 3), "unit": "GFlop/s", "cores": cores, "kind": "reference",
+                             "sample": sample, "host": host_info(),
+                             "step_ms": {"median": round(statistics.median(times) * 1e3, 3),
+                                         "min": round(min(times) * 1e3, 3), "max": round(max(times) * 1e3, 3)}},
+            "e2e": {"value": round(gf, 3), "unit": "GFlop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--devices", default="", help="comma-separated CUDA ordinals this process drives "
+                                                   "(default: 0..gpus-1, or LOCAL_RANK under torchrun)")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip the non-headline configs")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / parity leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer (e2e) legs")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -317,75 +489,106 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    dims3, n, dtype, batch = WORKLOADS[HEADLINE]
-    fl_e, by_e = flops_per_entry(dims3, n), bytes_per_entry(dims3, n, dtype)
-
     if args.impl == "reference":
-        if rank != 0:
-            return 0
-        gf, cores, sample, med = cpu_reference_sample(HEADLINE, seconds_budget=max(2.0, 0.5 * args.steps))
-        line = {"metric": METRIC, "value": round(gf, 3), "unit": "GFlop/s", "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": round(med * 1e3, 4), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generate_batch, seed 1)",
-                "impl": "reference",
-                "config": {"workload": f"{HEADLINE}: 2-D Kronecker action fp32 n=16 (reference CPU, bounded sample)",
-                           "batch_per_gpu": batch, "sample": sample},
-                "cpu_baseline": {"value": round(gf, 3), "unit": "GFlop/s", "cores": cores, "kind": "reference",
-                                 "sample": sample},
-                "e2e": {"value": round(gf, 3), "unit": "GFlop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return 0
+        return reference_arm(args, rank)
 
     import torch
 
-    torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo")  # host barrier + max over ranks only: no NCCL, no data-path collective
+        devices = [local]
+    elif args.devices:
+        devices = [int(d) for d in args.devices.split(",")]
+    else:
+        devices = list(range(args.gpus))
+    visible = torch.cuda.device_count()
+    if max(devices) >= visible:
+        print(json.dumps({"error": f"--gpus {args.gpus}: only {visible} CUDA device(s) visible; "
+                                   "pass --devices to reuse ordinals explicitly"}), flush=True)
+        return 2
+    torch.cuda.set_device(devices[0])
+    topo = Topo(devices, world, rank)
     import paper_1304_7054_b200 as kb
 
+    dims3, n, dtype, batch, scaling = WORKLOADS[HEADLINE]
+    fl_e, by_e = flops_per_entry(dims3, n), bytes_per_entry(dims3, n, dtype)
     hbm_peak, peak_kind = load_peaks()
     traffic = load_traffic()
-    with ClockSampler(local) as clk:
-        ms, launch_ms, launches, path = time_device(kb, torch, HEADLINE, args.steps, args.warmup, world, rank)
+    with ClockSampler(devices) as clk:
+        ms, launch_ms, launches, path, entries = time_device(kb, torch, topo, HEADLINE, args.steps, args.warmup)
     clocks = clk.summary()
-    value = fl_e * batch * world / (ms * 1e-3) / 1e9  # GFlop/s, whole job
-    gbs = by_e * batch * world / (ms * 1e-3) / 1e9
-    achieved = by_e * batch / (launch_ms * 1e-3) / 1e9  # per launch, this rank
-    e2e_ms, h2d, d2h = time_e2e(kb, torch, HEADLINE, args.e2e_steps, args.warmup, world)
-    e2e_value = fl_e * batch * world / (e2e_ms * 1e-3) / 1e9
+    total_entries = topo.sum(entries)
+    value = fl_e * total_entries / (ms * 1e-3) / 1e9  # GFlop/s, whole job
+    gbs = by_e * total_entries / (ms * 1e-3) / 1e9
+    per_part = batch
+    achieved = by_e * per_part / (launch_ms * 1e-3) / 1e9  # per launch, part 0
+
+    e2e = e2e_pg = None
+    host_bytes = 2 * by_e * batch * topo.parts  # X + Y + the pageable copies' worst case
+    try:
+        ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    except (ValueError, OSError):
+        ram = 1 << 40
+    if host_bytes > 0.35 * ram:
+        e2e = {"value": None, "skipped": f"host buffers ({host_bytes / 1e9:.0f} GB) exceed 35% of host RAM"}
+    elif not args.no_e2e:
+        e2e_ms, h2d, d2h = time_e2e(kb, torch, topo, HEADLINE, args.e2e_steps, args.warmup)
+        e2e = {"value": round(fl_e * total_entries / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GFlop/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
+               "buffers": "pinned host (torch pin_memory)"}
+        pg_ms, h2d, d2h = time_e2e(kb, torch, topo, HEADLINE, args.e2e_steps, args.warmup, pageable=True)
+        e2e_pg = {"value": round(fl_e * total_entries / (pg_ms * 1e-3) / 1e9, 1), "unit": "GFlop/s",
+                  "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(pg_ms, 3),
+                  "buffers": "pageable host (numpy), staged through pooled pinned bounce buffers",
+                  "vs_pinned": round(e2e_ms / pg_ms, 4)}
 
     extra = []
     if not args.no_extra:
         for name in WORKLOADS:
             if name == HEADLINE:
                 continue
-            d3, nn, dt, bt = WORKLOADS[name]
-            xms, xlaunch, _, xpath = time_device(kb, torch, name, max(5, args.steps // 2), args.warmup, world, rank)
+            d3, nn, dt, bt, sc = WORKLOADS[name]
             fe, be = flops_per_entry(d3, nn), bytes_per_entry(d3, nn, dt)
-            tf = fe * bt / (xlaunch * 1e-3) / 1e12
-            gb = be * bt / (xlaunch * 1e-3) / 1e9
+            l2 = torch.cuda.get_device_properties(devices[0]).L2_cache_size
+            sets = 1 if be * bt > 4 * l2 else -(-2 * l2 // (be * bt)) + 1  # rotate > 2x L2 of X/Y between launches
+            xms, xlaunch, _, xpath, xent = time_device(kb, torch, topo, name, max(5, args.steps // 2), args.warmup,
+                                                       sets)
+            xtotal = topo.sum(xent)
+            part0 = part_batch(topo, sc, bt, 0)
+            tf = fe * part0 / (xlaunch * 1e-3) / 1e12
+            gb = be * part0 / (xlaunch * 1e-3) / 1e9
             fpeak = FP32_PEAK_TFLOPS if dt == "f32" else FP64_PEAK_TFLOPS
             roof_tf = min(fpeak, hbm_peak * fe / be / 1e3)
-            rec = {"workload": name, "value": round(fe * bt * world / (xms * 1e-3) / 1e9, 1), "unit": "GFlop/s",
+            rec = {"workload": name, "scaling": sc, "entries_total": xtotal, "entries_per_gpu": part0,
+                   "value": round(fe * xtotal / (xms * 1e-3) / 1e9, 1), "unit": "GFlop/s",
                    "ms_per_step": round(xms, 4), "hbm_gbs": round(gb, 1), "kernel": xpath,
+                   "l2": ("inputs larger than L2" if sets == 1 else
+                          f"{sets} rotating X/Y sets ({sets * be * bt / 1e6:.0f} MB > 2x {l2 / 1e6:.0f} MB L2)"),
                    "roofline": {"bound": "hbm" if roof_tf < fpeak else "fp-pipe", "roof_tflops": round(roof_tf, 2),
                                 "frac": round(tf / roof_tf, 4), "hbm_frac": round(gb / hbm_peak, 4)}}
             if dt == "f32" and roof_tf >= fpeak:
                 rec["roofline"]["ffma2_peak_frac"] = round(tf / FFMA2_PEAK_TFLOPS, 4)
-            if bt * be < (256 << 20):  # small batch: host launch cost dominates -> also report a CUDA-graph replay
-                gms = time_graph(kb, torch, name, max(20, args.steps), world)
+            if bt * be < (256 << 20) and topo.parts == 1:  # small batch: host launch cost dominates
+                gms = time_graph(kb, torch, topo, name, max(20, args.steps), sets)
                 rec["cuda_graph"] = {"ms_per_launch": round(gms, 4),
-                                     "value": round(fe * bt * world / (gms * 1e-3) / 1e9, 1),
-                                     "hbm_gbs": round(be * bt / (gms * 1e-3) / 1e9, 1)}
+                                     "value": round(fe * xtotal / (gms * 1e-3) / 1e9, 1),
+                                     "hbm_gbs": round(be * part0 / (gms * 1e-3) / 1e9, 1),
+                                     "hbm_frac": round(be * part0 / (gms * 1e-3) / 1e9 / hbm_peak, 4)}
             extra.append(rec)
 
-    cpu = None
-    if rank == 0 and not args.no_cpu:
+    cpu = parity = None
+    if rank == 0 and world == 1 and len(devices) == 1 and not args.no_cpu:
         try:
-            gf, cores, sample, _ = cpu_reference_sample(HEADLINE)
-            cpu = {"value": round(gf, 3), "unit": "GFlop/s", "cores": cores, "kind": "reference", "sample": sample}
+            r = cpu_reference(HEADLINE, reps=10, parity=True)
+            cpu = {"value": round(r["gflops"], 3), "unit": "GFlop/s", "cores": r["cores"], "kind": "reference",
+                   "sample": f"full config: {r['batch']} entries (generate_batch seed 1), median of {r['reps']} reps, "
+                             f"OpenMP pinned ({', '.join(f'{k}={v}' for k, v in r['omp'].items())})",
+                   "same_config": r["full_batch"], "host": r["host"],
+                   "step_ms": {"median": round(r["median_s"] * 1e3, 3), "min": round(r["min_s"] * 1e3, 3),
+                               "max": round(r["max_s"] * 1e3, 3)}}
+            parity = r.get("parity")
         except Exception as e:  # reference .so missing on this box
             cpu = {"value": None, "unit": "GFlop/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -393,30 +596,36 @@ def main():
     if rank == 0:
         tr = traffic.get(HEADLINE)
         line = {
-            "metric": METRIC, "value": round(value, 1), "unit": "GFlop/s", "n_gpus": world if world > 1 else args.gpus,
+            "metric": METRIC, "value": round(value, 1), "unit": "GFlop/s", "n_gpus": topo.n_gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (torch uniform[-1,1), seed 1; inputs 4.3 GB/GPU >> 126 MB L2, no flush needed)",
+            "data": "synthetic (torch uniform[-1,1); inputs 4.3 GB/GPU >> 126 MB L2, no flush needed)",
             "config": {"workload": f"{HEADLINE}: 2-D Kronecker action Y=A X B^T, fp32, n=16, batch {batch} per GPU "
                                    "(BASELINE configs[1]), alpha 1 beta 0, tight layout",
-                       "batch_per_gpu": batch, "n": n, "l2": "inputs larger than L2"},
+                       "batch_per_gpu": batch, "n": n, "l2": "inputs larger than L2",
+                       "launch": (f"torchrun, {world} processes x 1 GPU, gloo host barrier" if world > 1 else
+                                  f"1 process, devices {devices}" + (" via kb.kron2_parts" if len(devices) > 1 else ""))},
             "hbm_gbs": round(gbs, 1),
             "kernel": path,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "peak_kind": peak_kind,
                          "traffic": tr if tr is None else tr.get("dram_bytes_per_launch"),
-                         "algorithmic_bytes_per_launch": by_e * batch},
-            "e2e": {"value": round(e2e_value, 1), "unit": "GFlop/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3)},
+                         "algorithmic_bytes_per_launch": by_e * per_part},
+            "e2e": e2e,
+            "e2e_pageable": e2e_pg,
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "parity": parity,
             "extra": extra,
         }
+        if len(devices) > 1:
+            line["devices"] = devices
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 

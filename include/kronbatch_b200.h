@@ -37,7 +37,9 @@
  *  - synchronous: Y is complete on return, unless exec->flags has
  *    KB_EXEC_ASYNC (device buffers only);
  *  - pointers may be device (cudaMalloc), managed, pinned host or pageable
- *    host memory; host buffers are staged through pooled device memory.
+ *    host memory; host buffers are staged through pooled device memory in
+ *    chunks whose copies overlap the kernels (pageable ones through pooled
+ *    pinned bounce buffers filled by several host threads).
  *
  * Return value: KB_OK or an error status; on error a NUL-terminated message
  * is written to err (if non-NULL) with the reference's exact wording, e.g.
@@ -70,14 +72,35 @@ enum {
                               also enabled process-wide by the environment variable KB_TF32=1 */
 
 /* Execution options; pass NULL for the defaults (current device, library
- * stream, synchronous). */
+ * stream, synchronous).
+ *
+ * Ordering: the library streams are blocking streams, so a call is ordered
+ * after work the caller queued on the legacy default stream (stream 0) of the
+ * buffers' device; with an explicit `stream` it is ordered on that stream.
+ * Device-resident X/Y always run on the device they live on (a batch that is
+ * already split over several GPUs goes through kb_*_parts below). */
 typedef struct kb_exec {
-  int32_t ndevices;       /* >1: shard the batch over devices[] by contiguous
-                             slices (host-resident X/Y); 0/1: single device */
+  int32_t ndevices;       /* >1: shard a HOST-resident batch over devices[] by
+                             contiguous slices [g*ceil(B/G), ...), one host
+                             worker per slice, joined before return (host
+                             barrier, no collective); 0/1: single device */
   const int32_t* devices; /* CUDA ordinals; NULL => current device */
   void* stream;           /* cudaStream_t for single-device calls; NULL => library stream */
   uint32_t flags;         /* KB_EXEC_* */
 } kb_exec;
+
+/* One part of a batch that is split over several GPUs (kb_*_parts). */
+typedef struct kb_part {
+  int32_t device;      /* GPU that runs the part: must be where X / Y live when
+                          they are device memory; host-resident parts are staged
+                          through this device */
+  int64_t batch_count; /* entries in this part */
+  const void* X;       /* entry 0 of the part (float* / double* per entry point) */
+  int64_t lenx;        /* addressable elements from X */
+  void* Y;
+  int64_t leny;
+  void* stream;        /* cudaStream_t on `device`; NULL => library stream */
+} kb_part;
 
 /* Y^p <- alpha * op(A) * op(X^p) * op(B)^T + beta * Y^p,  p < batch_count
  * (kron2.hpp:23-36). */
@@ -107,6 +130,35 @@ int kb_dkron3(char transa, char transb, char transc, int64_t m_a, int64_t n_a, i
               int64_t lenc, const double* X, int64_t ldx, int64_t ldx2, int64_t ldxp, int64_t lenx, double beta,
               double* Y, int64_t ldy, int64_t ldy2, int64_t ldyp, int64_t leny, double* work,
               int64_t work_capacity, const kb_exec* exec, char* err, size_t errlen);
+
+/* Multi-GPU form of kb_?kron2 / kb_?kron3 for batches that are already split
+ * over devices (one device-resident slice per GPU, as a data-parallel caller
+ * holds them). Same problem arguments as the single-call entry points; the
+ * per-part X / Y / batch_count / device / stream come from parts[]. Every part
+ * is validated before anything runs (errors are prefixed "part <i>: "), the
+ * parts run concurrently, one per device, and the call returns when all are
+ * done -- or, with KB_EXEC_ASYNC in flags and device-resident parts, once
+ * all are queued on their streams. No collective, no peer traffic. kron3 takes
+ * no workspace here (the sm_100a path never uses one). Bit-identical to one
+ * call over the concatenated batch. */
+int kb_skron2_parts(char transa, char transb, char transx, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+                    float alpha, const float* A, int64_t lda, int64_t lena, const float* B, int64_t ldb,
+                    int64_t lenb, int64_t ldx, int64_t ldxp, float beta, int64_t ldy, int64_t ldyp, int32_t nparts,
+                    const kb_part* parts, uint32_t flags, char* err, size_t errlen);
+int kb_dkron2_parts(char transa, char transb, char transx, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+                    double alpha, const double* A, int64_t lda, int64_t lena, const double* B, int64_t ldb,
+                    int64_t lenb, int64_t ldx, int64_t ldxp, double beta, int64_t ldy, int64_t ldyp, int32_t nparts,
+                    const kb_part* parts, uint32_t flags, char* err, size_t errlen);
+int kb_skron3_parts(char transa, char transb, char transc, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+                    int64_t m_c, int64_t n_c, float alpha, const float* A, int64_t lda, int64_t lena, const float* B,
+                    int64_t ldb, int64_t lenb, const float* C, int64_t ldc, int64_t lenc, int64_t ldx, int64_t ldx2,
+                    int64_t ldxp, float beta, int64_t ldy, int64_t ldy2, int64_t ldyp, int32_t nparts,
+                    const kb_part* parts, uint32_t flags, char* err, size_t errlen);
+int kb_dkron3_parts(char transa, char transb, char transc, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b,
+                    int64_t m_c, int64_t n_c, double alpha, const double* A, int64_t lda, int64_t lena,
+                    const double* B, int64_t ldb, int64_t lenb, const double* C, int64_t ldc, int64_t lenc,
+                    int64_t ldx, int64_t ldx2, int64_t ldxp, double beta, int64_t ldy, int64_t ldy2, int64_t ldyp,
+                    int32_t nparts, const kb_part* parts, uint32_t flags, char* err, size_t errlen);
 
 /* y^p <- alpha * op(A) * x^p + beta * y^p,  p < batch_count (kron1.hpp:9-16),
  * replaces kronbatch::kron1<float|double> (proj/include/kronbatch/kron1.hpp:17-62).
@@ -146,8 +198,11 @@ uint64_t kb_launch_count(void);
 /* name of the kernel the last call on this thread launched ("" if none):
  * "kron2_fast", "kron2_generic", "kron3_fast", "kron3_generic", "kron1", "gemm_a", "scale" */
 const char* kb_last_path(void);
-/* release pooled device / pinned buffers held by the calling thread */
+/* release the pooled device / pinned buffers and streams of every idle lane
+ * (all devices; lanes of calls in flight are kept) */
 void kb_release_buffers(void);
+/* device bytes currently held by the pool on `device` (-1: all devices) */
+uint64_t kb_pooled_bytes(int device);
 
 #ifdef __cplusplus
 }

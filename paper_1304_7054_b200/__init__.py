@@ -16,6 +16,7 @@ from .api import (  # noqa: F401
     KronProblem3D,
     MatrixOp,
     MatrixView,
+    Part,
     VectorView,
     Workspace,
     footprint,
@@ -23,11 +24,14 @@ from .api import (  # noqa: F401
     is_transposed,
     kron1,
     kron2,
+    kron2_parts,
     kron3,
+    kron3_parts,
     kron3_workspace_size,
     last_path,
     launch_count,
     op_dims,
+    pooled_bytes,
     release_buffers,
     validate,
     validate_batch,
@@ -35,7 +39,7 @@ from .api import (  # noqa: F401
 )
 
 __all__ = [
-    "Array3View", "BatchView", "Exec", "KronProblem2D", "KronProblem3D", "MatrixOp", "MatrixView", "VectorView",
-    "Workspace", "footprint", "gemm_a", "is_transposed", "kron1", "kron2", "kron3", "kron3_workspace_size", "last_path", "launch_count", "op_dims",
-    "release_buffers", "validate", "validate_batch", "version",
+    "Array3View", "BatchView", "Exec", "KronProblem2D", "KronProblem3D", "MatrixOp", "MatrixView", "Part", "VectorView",
+    "Workspace", "footprint", "gemm_a", "is_transposed", "kron1", "kron2", "kron2_parts", "kron3", "kron3_parts", "kron3_workspace_size", "last_path", "launch_count", "op_dims",
+    "pooled_bytes", "release_buffers", "validate", "validate_batch", "version",
 ]

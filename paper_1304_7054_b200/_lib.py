@@ -31,6 +31,11 @@ ABI_SYMBOLS = (
     "kb_launch_count",
     "kb_last_path",
     "kb_release_buffers",
+    "kb_pooled_bytes",
+    "kb_skron2_parts",
+    "kb_dkron2_parts",
+    "kb_skron3_parts",
+    "kb_dkron3_parts",
 )
 
 
@@ -40,6 +45,18 @@ class KbExec(C.Structure):
         ("devices", C.POINTER(C.c_int32)),
         ("stream", C.c_void_p),
         ("flags", C.c_uint32),
+    ]
+
+
+class KbPart(C.Structure):
+    _fields_ = [
+        ("device", C.c_int32),
+        ("batch_count", C.c_int64),
+        ("X", C.c_void_p),
+        ("lenx", C.c_int64),
+        ("Y", C.c_void_p),
+        ("leny", C.c_int64),
+        ("stream", C.c_void_p),
     ]
 
 
@@ -75,6 +92,19 @@ def _load(path: str = LIB_PATH):
         f.restype = C.c_int
         f.argtypes = [ch, ch, i64, i64, i64, i64, T, vp, i64, i64, i64, vp, i64, i64, T, vp, i64, i64, i64,
                       C.POINTER(KbExec), C.c_char_p, C.c_size_t]
+    u32, i32 = C.c_uint32, C.c_int32
+    for name, T in (("kb_skron2_parts", C.c_float), ("kb_dkron2_parts", C.c_double)):
+        f = getattr(lib, name)
+        f.restype = C.c_int
+        f.argtypes = [ch, ch, ch, i64, i64, i64, i64, T, vp, i64, i64, vp, i64, i64, i64, i64, T, i64, i64, i32,
+                      C.POINTER(KbPart), u32, C.c_char_p, C.c_size_t]
+    for name, T in (("kb_skron3_parts", C.c_float), ("kb_dkron3_parts", C.c_double)):
+        f = getattr(lib, name)
+        f.restype = C.c_int
+        f.argtypes = [ch, ch, ch, i64, i64, i64, i64, i64, i64, T, vp, i64, i64, vp, i64, i64, vp, i64, i64, i64, i64,
+                      i64, T, i64, i64, i64, i32, C.POINTER(KbPart), u32, C.c_char_p, C.c_size_t]
+    lib.kb_pooled_bytes.restype = C.c_uint64
+    lib.kb_pooled_bytes.argtypes = [C.c_int]
     lib.kb_kron3_workspace_size.restype = C.c_int
     lib.kb_kron3_workspace_size.argtypes = [i64, i64, i64, i64, C.POINTER(i64), C.c_char_p, C.c_size_t]
     lib.kb_version.restype = C.c_char_p

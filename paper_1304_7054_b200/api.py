@@ -481,6 +481,95 @@ def gemm_a(op_a, op_b, m: int, n: int, k: int, alpha, a: BatchView, b: MatrixVie
           a.base.len, pb or None, b.ld, b.len, beta, pc or None, c.base.ld, c.batch_stride, c.base.len, exec_=exec_)
 
 
+# -------------------------------------------------- multi-device parts ----
+
+@dataclass
+class Part:
+    """One part of a batch split over GPUs (kb_part): the part's X / Y batch
+    views (same entry layout in every part), the GPU that runs it (where its
+    device buffers live) and an optional CUDA stream on that GPU."""
+
+    device: int
+    x: BatchView
+    y: BatchView
+    stream: Any = None
+
+
+def _parts_c(parts: Sequence[Part], ctx: str):
+    if not parts:
+        return (_lib.KbPart * 1)(), 0, []
+    x0, y0 = parts[0].x, parts[0].y
+    arr = (_lib.KbPart * len(parts))()
+    ptrs = []
+    for i, p in enumerate(parts):
+        for v, v0, nm in ((p.x, x0, "X"), (p.y, y0, "Y")):
+            same = (type(v.base) is type(v0.base) and v.batch_stride == v0.batch_stride and
+                    getattr(v.base, "ld", None) == getattr(v0.base, "ld", None) and
+                    getattr(v.base, "ld2", None) == getattr(v0.base, "ld2", None))
+            if not same:
+                _layout_error(ctx, f"part {i}: {nm} entry layout differs from part 0")
+        _require(p.x.batch_count == p.y.batch_count, ctx, f"part {i}: X and Y batch_count differ")
+        (px, py), dt = _ptrs_and_dtype(p.x.base, p.y.base)
+        ptrs.append(dt)
+        s = p.stream
+        if s is not None and hasattr(s, "cuda_stream"):
+            s = s.cuda_stream
+        arr[i] = _lib.KbPart(int(p.device), int(p.x.batch_count), px or None, int(p.x.base.len), py or None,
+                             int(p.y.base.len), C.c_void_p(s) if s else None)
+    if len(set(ptrs)) > 1:
+        raise TypeError("all parts share one element type")
+    return arr, len(parts), ptrs
+
+
+def _parts_call(fn, *args, nparts, arr, asynchronous):
+    err = getattr(_ERR, "buf", None)
+    if err is None:
+        err = _ERR.buf = C.create_string_buffer(1024)
+    rc = fn(*args, nparts, arr, _lib.KB_EXEC_ASYNC if asynchronous else 0, err, 1024)
+    if rc:
+        _lib.raise_for(rc, err)
+
+
+def kron2_parts(pr: KronProblem2D, a: MatrixView, b: MatrixView, parts: Sequence[Part],
+                asynchronous: bool = False) -> None:
+    """kron2 over a batch already split across GPUs (kb_?kron2_parts): every part
+    validated first, then all parts run concurrently, one per device, with no
+    collective; returns when all are done (or all are queued, asynchronous)."""
+    arr, n, dts = _parts_c(parts, "kron2")
+    if n == 0:
+        return
+    x0, y0 = parts[0].x, parts[0].y
+    kron2(pr, a, b, BatchView(x0.base, 0, x0.batch_stride), BatchView(y0.base, 0, y0.batch_stride))  # shape checks
+    (pa, pb), _ = _ptrs_and_dtype(a, b)
+    fn = _lib.lib.kb_skron2_parts if dts[0] == "float32" else _lib.lib.kb_dkron2_parts
+    _parts_call(fn, _opc(pr.op_a), _opc(pr.op_b), _opc(pr.op_x), pr.m_a, pr.n_a, pr.m_b, pr.n_b, pr.alpha,
+                pa or None, a.ld, a.len, pb or None, b.ld, b.len, x0.base.ld, x0.batch_stride, pr.beta, y0.base.ld,
+                y0.batch_stride, nparts=n, arr=arr, asynchronous=asynchronous)
+
+
+def kron3_parts(pr: KronProblem3D, a: MatrixView, b: MatrixView, c: MatrixView, parts: Sequence[Part],
+                asynchronous: bool = False) -> None:
+    """kron3 over a batch already split across GPUs (kb_?kron3_parts); no
+    workspace (the sm_100a path never uses one)."""
+    arr, n, dts = _parts_c(parts, "kron3")
+    if n == 0:
+        return
+    x0, y0 = parts[0].x, parts[0].y
+    kron3(pr, a, b, c, BatchView(x0.base, 0, x0.batch_stride), BatchView(y0.base, 0, y0.batch_stride),
+          Workspace(None, 0))  # shape checks (batch 0: nothing runs)
+    (pa, pb, pc), _ = _ptrs_and_dtype(a, b, c)
+    fn = _lib.lib.kb_skron3_parts if dts[0] == "float32" else _lib.lib.kb_dkron3_parts
+    _parts_call(fn, _opc(pr.op_a), _opc(pr.op_b), _opc(pr.op_c), pr.m_a, pr.n_a, pr.m_b, pr.n_b, pr.m_c, pr.n_c,
+                pr.alpha, pa or None, a.ld, a.len, pb or None, b.ld, b.len, pc or None, c.ld, c.len, x0.base.ld,
+                x0.base.ld2, x0.batch_stride, pr.beta, y0.base.ld, y0.base.ld2, y0.batch_stride, nparts=n, arr=arr,
+                asynchronous=asynchronous)
+
+
+def pooled_bytes(device: int = -1) -> int:
+    """Device bytes held by the library's buffer pool (idle lanes) on `device` (-1: all)."""
+    return int(_lib.lib.kb_pooled_bytes(device))
+
+
 def launch_count() -> int:
     """Kernels this process has launched through libkronbatch_b200 (all devices)."""
     return int(_lib.lib.kb_launch_count())

@@ -230,11 +230,9 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
         bulk_g2s(dst + e * ITEM + n * PS, p.X + (first + e) * p.sx + (long long)n * NN, NN * sizeof(T), &bars[stage]);
       }
     } else if (tid == 0) {
-      const uintptr_t a0 = reinterpret_cast<uintptr_t>(p.X + first * p.sx) & ~uintptr_t(15);
-      const uintptr_t a1 =
-          (reinterpret_cast<uintptr_t>(p.X + (first + valid) * p.sx) + uintptr_t(15)) & ~uintptr_t(15);
-      mbar_arrive_expect_tx(&bars[stage], (unsigned)(a1 - a0));
-      bulk_g2s(dst, reinterpret_cast<const void*>(a0), (unsigned)(a1 - a0), &bars[stage]);
+      uintptr_t lo, hi;
+      group_span(p.X, p.batch, p.sx, first, valid, lo, hi);
+      span_g2s<T>(dst, lo, hi, &bars[stage]);
     }
   };
 

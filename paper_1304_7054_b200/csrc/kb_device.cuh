@@ -111,6 +111,45 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
 // order this thread's generic-proxy smem accesses before later async-proxy (TMA) writes
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
+// One thread lands global bytes [lo, hi) (element-aligned) in shared memory so
+// that global address a goes to dst + (a - (lo & ~15)); dst is 16-byte aligned.
+// Only [lo, hi) is read: the 16-byte-aligned interior by one bulk copy that
+// completes on `bar` (the arrive carries its byte count), the unaligned head
+// and tail (< 16 bytes each: only at the ends of a batch) by plain loads
+// stored BEFORE the arrive, whose release / the waiters' acquire publishes them
+// together with the bulk bytes.
+template <typename T>
+__device__ __forceinline__ void span_g2s(void* dst, uintptr_t lo, uintptr_t hi, unsigned long long* bar) {
+  const uintptr_t base = lo & ~uintptr_t(15);
+  const uintptr_t i0 = (lo + 15) & ~uintptr_t(15), i1 = hi & ~uintptr_t(15);
+  char* d = static_cast<char*>(dst);
+  if (i0 != lo || i1 != hi) {
+    const uintptr_t h1 = i0 < hi ? i0 : hi;
+    for (uintptr_t a = lo; a < h1; a += sizeof(T))
+      *reinterpret_cast<T*>(d + (a - base)) = *reinterpret_cast<const T*>(a);
+    for (uintptr_t a = i1 > h1 ? i1 : h1; a < hi; a += sizeof(T))
+      *reinterpret_cast<T*>(d + (a - base)) = *reinterpret_cast<const T*>(a);
+    fence_proxy_async();  // these generic writes before later TMA refills of the stage
+  }
+  const unsigned bulk = i1 > i0 ? static_cast<unsigned>(i1 - i0) : 0u;
+  mbar_arrive_expect_tx(bar, bulk);
+  if (bulk) bulk_g2s(d + (i0 - base), reinterpret_cast<const void*>(i0), bulk, bar);
+}
+
+// Span of a group of contiguous entries [first, first + count) (stride sx) of a
+// batch of `batch` entries at X: rounded out to 16 bytes for the bulk copy,
+// clamped to the batch's own bytes [X, X + batch*sx) so that nothing before the
+// first or after the last entry is read.
+template <typename T>
+__device__ __forceinline__ void group_span(const T* X, long long batch, long long sx, long long first, long long count,
+                                           uintptr_t& lo, uintptr_t& hi) {
+  const uintptr_t xb = reinterpret_cast<uintptr_t>(X), xe = reinterpret_cast<uintptr_t>(X + batch * sx);
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(X + first * sx) & ~uintptr_t(15);
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(X + (first + count) * sx) + uintptr_t(15)) & ~uintptr_t(15);
+  lo = a0 > xb ? a0 : xb;
+  hi = a1 < xe ? a1 : xe;
+}
+
 // Vector load of W consecutive elements (W*sizeof(T) bytes, naturally aligned).
 template <int W, typename T>
 __device__ __forceinline__ void lds_vec(T* dst, const T* src) {

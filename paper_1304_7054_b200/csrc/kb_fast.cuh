@@ -421,10 +421,9 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
       if (lane < valid) bulk_g2s(dst + lane * C::SLOT, p.X + (first + lane) * p.sx, NN * sizeof(T), &wbar[stage]);
     } else if (span) {
       if (lane == 0) {
-        const uintptr_t a0 = reinterpret_cast<uintptr_t>(p.X + first * NN) & ~uintptr_t(15);
-        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p.X + (first + valid) * NN) + uintptr_t(15)) & ~uintptr_t(15);
-        mbar_arrive_expect_tx(&wbar[stage], (unsigned)(a1 - a0));
-        bulk_g2s(dst, reinterpret_cast<const void*>(a0), (unsigned)(a1 - a0), &wbar[stage]);
+        uintptr_t lo, hi;
+        group_span(p.X, p.batch, (long long)NN, first, valid, lo, hi);
+        span_g2s<T>(dst, lo, hi, &wbar[stage]);
       }
     } else {
       constexpr int CPI = NN / VXC;  // chunks per entry

@@ -19,13 +19,12 @@
 #include <type_traits>
 #include <mutex>
 #include <string>
-#include <thread>
-#include <unordered_map>
 #include <vector>
 
 #include <cuda_runtime.h>
 
 #include "../../include/kronbatch_b200.h"
+#include "kb_devmgr.h"
 #include "kb_kernels.h"
 
 namespace {
@@ -39,10 +38,8 @@ thread_local std::string t_last_path;
 
 // ------------------------------------------------------------ errors -----
 
-struct Fail {
-  int code;
-  std::string msg;
-};
+using kbrt::Fail;
+using kbrt::cuda_check;
 
 int report(const Fail& f, char* err, size_t errlen) {
   if (err && errlen) {
@@ -56,14 +53,6 @@ std::string nums(i64 a, i64 b) { return "(" + std::to_string(a) + ") < (" + std:
 
 [[noreturn]] void layout_error(const std::string& ctx, const std::string& what) {
   throw Fail{KB_EINVAL, ctx.empty() ? what : ctx + ": " + what};
-}
-
-void cuda_check(cudaError_t e, const char* ctx) {
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    throw Fail{e == cudaErrorMemoryAllocation ? KB_ENOMEM : KB_ECUDA,
-               std::string(ctx) + ": CUDA error: " + cudaGetErrorString(e)};
-  }
 }
 
 // ------------------------------------------- validation (views.hpp) -----
@@ -105,92 +94,15 @@ void check_op(const char* ctx, char op) {
 }
 
 // ------------------------------------------------ device-buffer manager ---
+// Lanes (pooled streams + buffers per device), the shard task pool and the
+// copy pool live in kb_devmgr.{h,cu}.
 
-struct Buf {
-  void* p = nullptr;
-  size_t cap = 0;
-  void* get(size_t bytes) {
-    if (bytes <= cap) return p;
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-    const size_t want = std::max(bytes, cap * 3 / 2);
-    cuda_check(cudaMalloc(&p, want), "device buffer");
-    cap = want;
-    return p;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-  }
-};
-
-constexpr int kSlots = 4;  // staged pipeline streams / buffer slots allocated per device
-
-// Staged pipeline shape: chunks in flight (<= kSlots) and MiB of X+Y per
-// chunk; KB_STAGE_SLOTS / KB_STAGE_MB override the defaults for sweeps.
-int stage_slots() {
-  static const int v = [] {
-    const char* e = std::getenv("KB_STAGE_SLOTS");
-    const int n = e ? std::atoi(e) : 3;
-    return n < 1 ? 1 : (n > kSlots ? kSlots : n);
-  }();
-  return v;
-}
-long long stage_bytes() {
-  static const long long v = [] {
-    const char* e = std::getenv("KB_STAGE_MB");
-    const long long mb = e ? std::atoll(e) : 128;
-    return (mb < 1 ? 1 : mb) << 20;
-  }();
-  return v;
-}
-
-struct DevRes {
-  int device = -1;
-  int sm_count = 0;
-  cudaStream_t stream = nullptr;        // library stream
-  cudaStream_t slot_stream[kSlots] = {};  // staged pipeline streams
-  Buf consts;
-  Buf scratch[kSlots];
-  Buf xs[kSlots], ys[kSlots];
-};
-
-struct ThreadRes {
-  std::unordered_map<int, DevRes*> by_dev;
-  ~ThreadRes() {
-    // streams/buffers are intentionally not destroyed at thread exit: the CUDA
-    // runtime may already be torn down at process exit (kb_release_buffers()
-    // frees them explicitly).
-  }
-};
-thread_local ThreadRes t_res;
-
-DevRes& dev_res(int dev) {
-  auto it = t_res.by_dev.find(dev);
-  if (it != t_res.by_dev.end()) return *it->second;
-  auto* r = new DevRes;
-  r->device = dev;
-  cuda_check(cudaDeviceGetAttribute(&r->sm_count, cudaDevAttrMultiProcessorCount, dev), "device query");
-  cuda_check(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking), "stream");
-  for (auto& s : r->slot_stream) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-  t_res.by_dev[dev] = r;
-  return *r;
-}
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (dev != prev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
+using kbrt::DeviceGuard;
+using kbrt::Lane;
+using kbrt::LaneLease;
+using kbrt::kSlots;
+using kbrt::stage_bytes;
+using kbrt::stage_slots;
 
 // ---------------------------------------------------- pointer classes ----
 
@@ -291,7 +203,7 @@ struct K2 {
 // Launch the compute for entries [0, n) of device-resident X/Y views.
 template <typename T, typename Upload>
 void run2_device(const K2<T>& k, const T* A, const T* B, const T* ha, const T* hw, const T* X, T* Y, i64 n,
-                 DevRes& r, cudaStream_t s, int slot, Upload&& upload) {
+                 Lane& r, cudaStream_t s, int slot, Upload&& upload) {
   Kron2Params<T> p{};
   p.A = A; p.B = B; p.X = X; p.Y = Y;
   p.lda = k.lda; p.ldb = k.ldb; p.ldx = k.ldx; p.sx = k.sx; p.ldy = k.ldy; p.sy = k.sy;
@@ -321,7 +233,7 @@ void run2_device(const K2<T>& k, const T* A, const T* B, const T* ha, const T* h
 }
 
 template <typename T>
-void scale2_device(const K2<T>& k, T* Y, i64 n, DevRes& r, cudaStream_t s) {
+void scale2_device(const K2<T>& k, T* Y, i64 n, Lane& r, cudaStream_t s) {
   const int mode = beta_mode_of((double)k.beta);
   if (mode == kb::kBetaOne) return;  // Y <- Y (reference rewrites the same value)
   const int grid = (int)std::max<i64>(1, std::min<i64>((n * k.m_a * k.m_b + 255) / 256, (i64)r.sm_count * 16));
@@ -338,16 +250,33 @@ struct StageSpec {
   bool y_in;             // copy Y span in before compute (beta != 0 or padded Y)
   bool x_used;           // X is read
   size_t es;             // element size
+  bool x_pageable = false, y_pageable = false;  // host buffers not page-locked: bounce through pinned memory
 };
 
-// `prep(res, stream)` runs once per slice before any compute (constant
-// upload); `compute(Xd, Yd, n, res, stream, slot)` launches the kernel(s).
+// `prep(lane, stream)` runs once per slice before any compute (constant
+// upload); `compute(Xd, Yd, n, lane, stream, slot)` launches the kernel(s).
+//
+// Device-resident X/Y: one launch on the caller's stream (or the lane's
+// library stream), in place. Host-resident X and/or Y: the slice is cut into
+// chunks of ~stage_bytes() of X+Y that rotate over stage_slots() streams, so
+// the H2D copy of chunk c+1, the kernel on chunk c and the D2H copy of chunk
+// c-1 overlap. Page-locked host buffers are the DMA source/target directly;
+// pageable ones go through the lane's pinned bounce buffers, filled and
+// drained by the copy pool (several host threads) while the GPU works on the
+// neighbouring chunks -- so a std::vector caller keeps the copy engines busy
+// instead of serialising on the driver's internal staging.
 template <typename Prep, typename Compute>
 void run_slice(int dev, const void* X, void* Y, i64 p0, i64 p1, const StageSpec& sp, bool x_dev, bool y_dev,
                cudaStream_t user_stream, bool sync, Prep&& prep, Compute&& compute) {
-  DeviceGuard g(dev);
-  DevRes& r = dev_res(dev);
   if (p1 <= p0) return;
+  DeviceGuard g(dev);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (user_stream && cudaStreamIsCapturing(user_stream, &cap) != cudaSuccess) {
+    cudaGetLastError();
+    cap = cudaStreamCaptureStatusNone;
+  }
+  LaneLease lease(dev, cap != cudaStreamCaptureStatusNone);
+  Lane& r = *lease.lane;
   const char* Xb = static_cast<const char*>(X);
   char* Yb = static_cast<char*>(Y);
   if ((x_dev || !sp.x_used) && y_dev) {
@@ -355,49 +284,99 @@ void run_slice(int dev, const void* X, void* Y, i64 p0, i64 p1, const StageSpec&
     prep(r, s);
     compute(sp.x_used ? Xb + sp.es * (size_t)(p0 * sp.sx) : nullptr, Yb + sp.es * (size_t)(p0 * sp.sy), p1 - p0, r,
             s, 0);
-    if (sync) cuda_check(cudaStreamSynchronize(s), "synchronize");
+    if (sync)
+      cuda_check(cudaStreamSynchronize(s), "synchronize");
+    else
+      lease.async_stream = s;  // pooled constants / scratch stay busy until this stream passes the call
     return;
   }
   prep(r, r.slot_stream[0]);
   cuda_check(cudaStreamSynchronize(r.slot_stream[0]), "synchronize");
-  // staged: chunk so one slot holds ~64 MiB of X+Y
   const i64 per_entry = (sp.x_used && !x_dev ? sp.sx : 0) + (!y_dev ? sp.sy : 0);
   const i64 target = stage_bytes() / (i64)sp.es;
   const int nslots = stage_slots();
   i64 chunk = std::max<i64>(1, per_entry > 0 ? target / per_entry : (p1 - p0));
   chunk = std::min(chunk, p1 - p0);
   if (user_stream) cuda_check(cudaStreamSynchronize(user_stream), "synchronize");
+  const bool x_bounce = sp.x_used && !x_dev && sp.x_pageable;
+  const bool y_bounce = !y_dev && sp.y_pageable;
+  struct InFlight {
+    bool live = false;
+    char* ydst = nullptr;  // caller's Y span of the chunk (bounced Y only)
+    size_t ybytes = 0;
+  } fl[kSlots];
+  // Wait for the chunk that last used `slot`, and hand its bounced Y back to
+  // the caller's buffer (as a copy job, so it can share the pool with an X job).
+  auto retire = [&](int slot, std::vector<kbrt::CopyJob>& jobs) {
+    if (!fl[slot].live) return;
+    cuda_check(cudaStreamSynchronize(r.slot_stream[slot]), "synchronize");
+    if (y_bounce) jobs.push_back(kbrt::CopyJob{fl[slot].ydst, r.hy[slot].p, fl[slot].ybytes});
+    fl[slot].live = false;
+  };
+  // size the bounce buffers for a full chunk up front: a buffer must never be
+  // reallocated while it still holds a chunk's Y on its way back
+  for (int k = 0; k < nslots; ++k) {
+    if (x_bounce) r.hx[k].get(sp.es * (size_t)((chunk - 1) * sp.sx + sp.fpx));
+    if (y_bounce) r.hy[k].get(sp.es * (size_t)((chunk - 1) * sp.sy + sp.fpy));
+  }
+  std::vector<kbrt::CopyJob> jobs;
   i64 c = 0;
   for (i64 q0 = p0; q0 < p1; q0 += chunk, ++c) {
     const i64 q1 = std::min(p1, q0 + chunk), n = q1 - q0;
     const int slot = (int)(c % nslots);
     cudaStream_t s = r.slot_stream[slot];
+    jobs.clear();
+    retire(slot, jobs);
+    const char* xsrc = sp.x_used ? Xb + sp.es * (size_t)(q0 * sp.sx) : nullptr;
+    const size_t xbytes = sp.x_used ? sp.es * (size_t)((n - 1) * sp.sx + sp.fpx) : 0;
+    char* ysrc = Yb + sp.es * (size_t)(q0 * sp.sy);
+    const size_t ybytes = sp.es * (size_t)((n - 1) * sp.sy + sp.fpy);
+    const char* xh = xsrc;  // DMA source of X (caller's pinned buffer or the bounce buffer)
+    char* yh = ysrc;        // DMA target of Y
+    if (x_bounce) {
+      void* hb = r.hx[slot].get(xbytes);
+      jobs.push_back(kbrt::CopyJob{hb, xsrc, xbytes});
+      xh = static_cast<const char*>(hb);
+    }
+    if (y_bounce) {
+      yh = static_cast<char*>(r.hy[slot].get(ybytes));
+      if (sp.y_in) {  // the retired chunk's Y must leave hy[slot] before this chunk's Y lands there
+        kbrt::parallel_copy(jobs.data(), (int)jobs.size());
+        jobs.clear();
+        jobs.push_back(kbrt::CopyJob{yh, ysrc, ybytes});
+      }
+    }
+    if (!jobs.empty()) kbrt::parallel_copy(jobs.data(), (int)jobs.size());
     const char* xd = nullptr;
     if (sp.x_used) {
-      const char* xsrc = Xb + sp.es * (size_t)(q0 * sp.sx);
       if (x_dev) {
         xd = xsrc;
       } else {
-        const size_t bytes = sp.es * (size_t)((n - 1) * sp.sx + sp.fpx);
-        void* d = r.xs[slot].get(bytes);
-        cuda_check(cudaMemcpyAsync(d, xsrc, bytes, cudaMemcpyHostToDevice, s), "X upload");
+        void* d = r.xs[slot].get(xbytes);
+        cuda_check(cudaMemcpyAsync(d, xh, xbytes, cudaMemcpyHostToDevice, s), "X upload");
         xd = static_cast<const char*>(d);
       }
     }
-    char* ysrc = Yb + sp.es * (size_t)(q0 * sp.sy);
     char* yd = ysrc;
-    const size_t ybytes = sp.es * (size_t)((n - 1) * sp.sy + sp.fpy);
     if (!y_dev) {
       yd = static_cast<char*>(r.ys[slot].get(ybytes));
-      if (sp.y_in) cuda_check(cudaMemcpyAsync(yd, ysrc, ybytes, cudaMemcpyHostToDevice, s), "Y upload");
+      if (sp.y_in) cuda_check(cudaMemcpyAsync(yd, yh, ybytes, cudaMemcpyHostToDevice, s), "Y upload");
     }
     compute(xd, yd, n, r, s, slot);
-    if (!y_dev) cuda_check(cudaMemcpyAsync(ysrc, yd, ybytes, cudaMemcpyDeviceToHost, s), "Y download");
+    if (!y_dev) cuda_check(cudaMemcpyAsync(yh, yd, ybytes, cudaMemcpyDeviceToHost, s), "Y download");
+    fl[slot] = InFlight{true, ysrc, ybytes};
   }
-  for (int k = 0; k < kSlots; ++k) cuda_check(cudaStreamSynchronize(r.slot_stream[k]), "synchronize");
+  // drain in chunk order so the last copies overlap the GPU's last chunks
+  const i64 nchunks = c;
+  for (i64 k = std::max<i64>(0, nchunks - nslots); k < nchunks; ++k) {
+    jobs.clear();
+    retire((int)(k % nslots), jobs);
+    if (!jobs.empty()) kbrt::parallel_copy(jobs.data(), (int)jobs.size());
+  }
 }
 
-// Shard [0, batch) over devices (contiguous slices), one host thread per GPU.
+// Shard [0, batch) over devices (contiguous slices [g*ceil(B/G), ...)), one
+// persistent pool thread per slice; returns when every slice is done.
 template <typename Slice>
 void shard(const kb_exec* exec, int default_dev, i64 batch, Slice&& slice) {
   std::vector<int> devs;
@@ -412,23 +391,10 @@ void shard(const kb_exec* exec, int default_dev, i64 batch, Slice&& slice) {
     return;
   }
   const i64 per = (batch + G - 1) / G;
-  std::vector<std::thread> th;
-  std::vector<Fail> fails(G, Fail{KB_OK, {}});
-  for (i64 g = 0; g < G; ++g) {
+  kbrt::parallel_tasks((int)G, [&](int g) {
     const i64 p0 = std::min(batch, g * per), p1 = std::min(batch, (g + 1) * per);
-    th.emplace_back([&, g, p0, p1] {
-      try {
-        slice(devs[g], p0, p1);
-      } catch (const Fail& f) {
-        fails[g] = f;
-      } catch (const std::exception& e) {
-        fails[g] = Fail{KB_EINTERNAL, e.what()};
-      }
-    });
-  }
-  for (auto& t : th) t.join();  // host barrier: the call returns with every slice done
-  for (auto& f : fails)
-    if (f.code != KB_OK) throw f;
+    slice(devs[(size_t)g], p0, p1);
+  });
 }
 
 int current_device() {
@@ -440,7 +406,8 @@ int current_device() {
 template <typename T>
 int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i64 batch, T alpha, const T* A,
                 i64 lda, i64 lena, const T* B, i64 ldb, i64 lenb, const T* X, i64 ldx, i64 ldxp, i64 lenx, T beta,
-                T* Y, i64 ldy, i64 ldyp, i64 leny, const kb_exec* exec, char* err, size_t errlen) {
+                T* Y, i64 ldy, i64 ldyp, i64 leny, const kb_exec* exec, char* err, size_t errlen,
+                bool dry = false) {
   t_last_path.clear();
   try {
     check_op("kron2: A", ta);
@@ -460,6 +427,7 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
     if (batch == 0 || m_a == 0 || m_b == 0) return KB_OK;
     const bool scale_only = alpha == T(0) || n_a == 0 || n_b == 0;  // kron2.hpp:67
     if (scale_only && beta == T(1)) return KB_OK;
+    if (dry) return KB_OK;  // validation only (kb_*_parts pre-pass)
 
     K2<T> k{ta, tb, tx, m_a, n_a, m_b, n_b, batch, alpha, beta, A, lda, B, ldb, X, ldx, ldxp, fpx, Y, ldy, ldyp, fpy};
     const bool square_fast = m_a == n_a && m_a == m_b && m_a == n_b && m_a >= 1 && m_a <= 16;
@@ -468,13 +436,15 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
     const int dev0 = y_dev ? yi.dev : (x_dev ? xi.dev : current_device());
     const bool y_tight = ldy == m_a && ldyp == m_a * m_b;
     StageSpec sp{ldxp, fpx, ldyp, fpy, beta != T(0) || !y_tight, !scale_only, sizeof(T)};
+    sp.x_pageable = !xi.device && !xi.pinned;
+    sp.y_pageable = !yi.device && !yi.pinned;
     cudaStream_t us = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
     const bool sync = !(exec && (exec->flags & KB_EXEC_ASYNC) && x_dev && y_dev);
     auto slice = [&](int dev, i64 p0, i64 p1) {
       const T* Ad = nullptr;
       const T* Bd = nullptr;
       std::vector<T> ha, hw;  // host-resolved constants for the square fast path
-      auto upload = [&](DevRes& r, cudaStream_t s) {
+      auto upload = [&](Lane& r, cudaStream_t s) {
         if (Ad) return;
         const i64 fa = fp_matrix(ac, lda), fb = fp_matrix(bc, ldb);
         T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + fb + 64)));
@@ -483,7 +453,7 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
       };
       run_slice(
           dev, X, Y, p0, p1, sp, x_dev && xi.dev == dev, y_dev && yi.dev == dev, us, sync,
-          [&](DevRes& r, cudaStream_t s) {
+          [&](Lane& r, cudaStream_t s) {
             if (scale_only) return;  // A, B never read (kron2.hpp:67-79)
             // device copies of A/B only feed the generic kernel (the fast
             // kernels take host-resolved constants as parameters)
@@ -494,7 +464,7 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
               hw = resolve_sq(fetch_host(B, fb, s), ldb, is_t(tb), (int)m_a, true, alpha, true);
             }
           },
-          [&](const void* xd, void* yd, i64 n, DevRes& r, cudaStream_t s, int slot) {
+          [&](const void* xd, void* yd, i64 n, Lane& r, cudaStream_t s, int slot) {
             if (scale_only)
               scale2_device<T>(k, static_cast<T*>(yd), n, r, s);
             else
@@ -549,6 +519,8 @@ int kron1_entry(char ta, i64 m_a, i64 n_a, i64 batch, T alpha, const T* A, i64 l
     const bool x_dev = !scale_only && xi.device, y_dev = yi.device;
     const int dev0 = y_dev ? yi.dev : (x_dev ? xi.dev : current_device());
     StageSpec sp{ldxp, n_a, ldyp, m_a, beta != T(0) || ldyp != m_a, !scale_only, sizeof(T)};
+    sp.x_pageable = !xi.device && !xi.pinned;
+    sp.y_pageable = !yi.device && !yi.pinned;
     cudaStream_t us = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
     const bool sync = !(exec && (exec->flags & KB_EXEC_ASYNC) && (x_dev || scale_only) && y_dev);
     const int bmode = beta_mode_of((double)beta);
@@ -560,7 +532,7 @@ int kron1_entry(char ta, i64 m_a, i64 n_a, i64 batch, T alpha, const T* A, i64 l
       std::vector<T> ha;
       run_slice(
           dev, X, Y, p0, p1, sp, x_dev && xi.dev == dev, y_dev && yi.dev == dev, us, sync,
-          [&](DevRes& r, cudaStream_t s) {
+          [&](Lane& r, cudaStream_t s) {
             if (scale_only) return;  // A, X never read (kron1.hpp:45-55)
             const i64 fa = fp_matrix(ac, lda);
             if (square_fast) {
@@ -570,7 +542,7 @@ int kron1_entry(char ta, i64 m_a, i64 n_a, i64 batch, T alpha, const T* A, i64 l
             T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + 32)));
             Ad = const_on_device(A, fa, r.device, cs, s);
           },
-          [&](const void* xd, void* yd, i64 n, DevRes& r, cudaStream_t s, int) {
+          [&](const void* xd, void* yd, i64 n, Lane& r, cudaStream_t s, int) {
             if (scale_only) {
               const int grid = (int)std::max<i64>(1, std::min<i64>((n * m_a + 255) / 256, (i64)r.sm_count * 16));
               cuda_check(kb::launch_scale<T>(static_cast<T*>(yd), n, m_a, 1, 1, m_a, 0, ldyp, bmode, beta, grid, s),
@@ -623,6 +595,8 @@ int gemm_a_entry(char ta, char tb, i64 m, i64 n, i64 k, i64 batch, T alpha, cons
     const bool a_dev = !scale_only && ai.device, c_dev = ci.device;
     const int dev0 = c_dev ? ci.dev : (a_dev ? ai.dev : current_device());
     StageSpec sp{ldap, fpa, ldcp, fpc, beta != T(0) || ldc != m || ldcp != m * n, !scale_only, sizeof(T)};
+    sp.x_pageable = !ai.device && !ai.pinned;
+    sp.y_pageable = !ci.device && !ci.pinned;
     cudaStream_t us = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
     const bool sync = !(exec && (exec->flags & KB_EXEC_ASYNC) && (a_dev || scale_only) && c_dev);
     const int bmode = beta_mode_of((double)beta);
@@ -636,7 +610,7 @@ int gemm_a_entry(char ta, char tb, i64 m, i64 n, i64 k, i64 batch, T alpha, cons
       std::vector<T> hw;
       run_slice(
           dev, A, Cm, p0, p1, sp, a_dev && ai.dev == dev, c_dev && ci.dev == dev, us, sync,
-          [&](DevRes& r, cudaStream_t s) {
+          [&](Lane& r, cudaStream_t s) {
             if (scale_only) return;  // A, B never read (gemm_a.hpp:46-58)
             const i64 fb = fp_matrix(bc, ldb);
             if (square_fast) {  // w(kk, c) = op(B)(kk, c), times alpha for gemm_axpy (detail.hpp:53)
@@ -646,7 +620,7 @@ int gemm_a_entry(char ta, char tb, i64 m, i64 n, i64 k, i64 batch, T alpha, cons
             T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fb + 32)));
             Bd = const_on_device(B, fb, r.device, cs, s);
           },
-          [&](const void* ad, void* cd, i64 nb, DevRes& r, cudaStream_t s, int) {
+          [&](const void* ad, void* cd, i64 nb, Lane& r, cudaStream_t s, int) {
             if (scale_only) {
               const int grid = (int)std::max<i64>(1, std::min<i64>((nb * m * n + 255) / 256, (i64)r.sm_count * 16));
               cuda_check(kb::launch_scale<T>(static_cast<T*>(cd), nb, m, n, 1, ldc, 0, ldcp, bmode, beta, grid, s),
@@ -684,7 +658,8 @@ template <typename T>
 int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i64 m_c, i64 n_c, i64 batch, T alpha,
                 const T* A, i64 lda, i64 lena, const T* B, i64 ldb, i64 lenb, const T* Cm, i64 ldc, i64 lenc,
                 const T* X, i64 ldx, i64 ldx2, i64 ldxp, i64 lenx, T beta, T* Y, i64 ldy, i64 ldy2, i64 ldyp,
-                i64 leny, T* work, i64 work_cap, const kb_exec* exec, char* err, size_t errlen) {
+                i64 leny, T* work, i64 work_cap, const kb_exec* exec, char* err, size_t errlen,
+                bool dry = false) {
   (void)work;
   t_last_path.clear();
   try {
@@ -716,6 +691,7 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
     if (batch == 0 || m_a == 0 || m_b == 0 || m_c == 0) return KB_OK;  // kron3.hpp:111
     const bool scale_only = alpha == T(0) || n_a == 0 || n_b == 0 || n_c == 0;  // kron3.hpp:113
     if (scale_only && beta == T(1)) return KB_OK;
+    if (dry) return KB_OK;
 
     Kron3Params<T> base{};
     base.lda = lda; base.ldb = ldb; base.ldc = ldc;
@@ -731,6 +707,8 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
     const int dev0 = y_dev ? yi.dev : (x_dev ? xi.dev : current_device());
     const bool y_tight = ldy == m_a && ldy2 == m_a * m_b && ldyp == m_a * m_b * m_c;
     StageSpec sp{ldxp, fpx, ldyp, fpy, beta != T(0) || !y_tight, !scale_only, sizeof(T)};
+    sp.x_pageable = !xi.device && !xi.pinned;
+    sp.y_pageable = !yi.device && !yi.pinned;
     cudaStream_t us = exec ? static_cast<cudaStream_t>(exec->stream) : nullptr;
     const bool sync = !(exec && (exec->flags & KB_EXEC_ASYNC) && x_dev && y_dev);
     const i64 fa = fp_matrix(ac, lda), fb = fp_matrix(bc, ldb), fc = fp_matrix(cc, ldc);
@@ -740,18 +718,18 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
     auto slice = [&](int dev, i64 p0, i64 p1) {
       const T *Ad = nullptr, *Bd = nullptr, *Cd = nullptr;
       std::vector<T> ha, hb, hc;  // host-resolved constants for the square fast path
-      DevRes* rp = nullptr;
+      Lane* rp = nullptr;
       cudaStream_t up_stream = nullptr;
       auto upload = [&]() {  // A/B/C on the device (in place when already resident)
         if (Ad) return;
-        DevRes& r = *rp;
+        Lane& r = *rp;
         T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + fb + fc + 96)));
         Ad = const_on_device(A, fa, r.device, cs, up_stream);
         Bd = const_on_device(B, fb, r.device, cs + fa + 32, up_stream);
         Cd = const_on_device(Cm, fc, r.device, cs + fa + fb + 64, up_stream);
       };
       run_slice(dev, X, Y, p0, p1, sp, x_dev && xi.dev == dev, y_dev && yi.dev == dev, us, sync,
-                [&](DevRes& r, cudaStream_t s) {
+                [&](Lane& r, cudaStream_t s) {
                   rp = &r;
                   up_stream = s;
                   if (scale_only) return;  // A, B, C never read (kron3.hpp:113-128)
@@ -765,7 +743,7 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                     hc = resolve_sq(fetch_host(Cm, fc, s), ldc, is_t(tc), (int)m_a, true, alpha, true);
                   }
                 },
-                [&](const void* xd, void* yd, i64 n, DevRes& r, cudaStream_t s, int slot) {
+                [&](const void* xd, void* yd, i64 n, Lane& r, cudaStream_t s, int slot) {
                   if (scale_only) {
                     const int mode = base.beta_mode;
                     const int grid = (int)std::max<i64>(
@@ -832,6 +810,44 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
     return report(f, err, errlen);
   } catch (const std::exception& e) {
     return report(Fail{KB_EINTERNAL, std::string("kron3: ") + e.what()}, err, errlen);
+  }
+}
+
+// ------------------------------------------------- multi-device parts -----
+// kb_{s,d}kron{2,3}_parts: one call over batch parts that already live on
+// (or are assigned to) different GPUs -- e.g. one device-resident slice per
+// GPU. Every part is validated first (nothing runs if any part is invalid);
+// then each part runs on its device through the single-device path, all parts
+// concurrently (one pool task per part), and the call returns when every part
+// is done (host barrier), or once every part is queued with KB_EXEC_ASYNC.
+// There is no collective: parts are independent.
+template <typename Entry>
+int run_parts(int32_t nparts, const kb_part* parts, uint32_t flags, char* err, size_t errlen, Entry&& entry) {
+  t_last_path.clear();
+  try {
+    if (nparts < 0 || (nparts > 0 && !parts)) throw Fail{KB_EINVAL, "parts: invalid part list"};
+    char buf[1024];
+    for (int32_t i = 0; i < nparts; ++i) {
+      const kb_exec ex{1, &parts[i].device, parts[i].stream, flags};
+      buf[0] = 0;
+      const int rc = entry(parts[i], &ex, buf, sizeof buf, true);
+      if (rc != KB_OK) throw Fail{rc, "part " + std::to_string(i) + ": " + buf};
+    }
+    std::vector<std::string> paths((size_t)std::max(nparts, 1));
+    kbrt::parallel_tasks(nparts, [&](int i) {
+      const kb_exec ex{1, &parts[i].device, parts[i].stream, flags};
+      char b[1024] = {0};
+      const int rc = entry(parts[i], &ex, b, sizeof b, false);
+      if (rc != KB_OK) throw Fail{rc, "part " + std::to_string(i) + ": " + b};
+      paths[(size_t)i] = t_last_path;
+    });
+    for (auto& p : paths)
+      if (!p.empty()) t_last_path = p;
+    return KB_OK;
+  } catch (const Fail& f) {
+    return report(f, err, errlen);
+  } catch (const std::exception& e) {
+    return report(Fail{KB_EINTERNAL, std::string("parts: ") + e.what()}, err, errlen);
   }
 }
 
@@ -925,22 +941,43 @@ uint64_t kb_launch_count(void) { return g_launches.load(std::memory_order_relaxe
 
 const char* kb_last_path(void) { return t_last_path.c_str(); }
 
-void kb_release_buffers(void) {
-  for (auto& kv : t_res.by_dev) {
-    DevRes* r = kv.second;
-    DeviceGuard g(r->device);
-    cudaDeviceSynchronize();
-    r->consts.release();
-    for (int i = 0; i < kSlots; ++i) {
-      r->scratch[i].release();
-      r->xs[i].release();
-      r->ys[i].release();
-      cudaStreamDestroy(r->slot_stream[i]);
-    }
-    cudaStreamDestroy(r->stream);
-    delete r;
+void kb_release_buffers(void) { kbrt::release_all_lanes(); }
+
+uint64_t kb_pooled_bytes(int device) { return (uint64_t)kbrt::pooled_device_bytes(device); }
+
+#define KB_PARTS2(NAME, T)                                                                                          \
+  int NAME(char transa, char transb, char transx, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b, T alpha,     \
+           const T* A, int64_t lda, int64_t lena, const T* B, int64_t ldb, int64_t lenb, int64_t ldx, int64_t ldxp, \
+           T beta, int64_t ldy, int64_t ldyp, int32_t nparts, const kb_part* parts, uint32_t flags, char* err,     \
+           size_t errlen) {                                                                                        \
+    return run_parts(nparts, parts, flags, err, errlen,                                                           \
+                     [&](const kb_part& p, const kb_exec* ex, char* e, size_t el, bool dry) {                      \
+                       return kron2_entry<T>(transa, transb, transx, m_a, n_a, m_b, n_b, p.batch_count, alpha, A,  \
+                                             lda, lena, B, ldb, lenb, static_cast<const T*>(p.X), ldx, ldxp,       \
+                                             p.lenx, beta, static_cast<T*>(p.Y), ldy, ldyp, p.leny, ex, e, el,     \
+                                             dry);                                                                 \
+                     });                                                                                           \
   }
-  t_res.by_dev.clear();
-}
+KB_PARTS2(kb_skron2_parts, float)
+KB_PARTS2(kb_dkron2_parts, double)
+
+#define KB_PARTS3(NAME, T)                                                                                          \
+  int NAME(char transa, char transb, char transc, int64_t m_a, int64_t n_a, int64_t m_b, int64_t n_b, int64_t m_c, \
+           int64_t n_c, T alpha, const T* A, int64_t lda, int64_t lena, const T* B, int64_t ldb, int64_t lenb,      \
+           const T* C, int64_t ldc, int64_t lenc, int64_t ldx, int64_t ldx2, int64_t ldxp, T beta, int64_t ldy,     \
+           int64_t ldy2, int64_t ldyp, int32_t nparts, const kb_part* parts, uint32_t flags, char* err,            \
+           size_t errlen) {                                                                                        \
+    return run_parts(nparts, parts, flags, err, errlen,                                                           \
+                     [&](const kb_part& p, const kb_exec* ex, char* e, size_t el, bool dry) {                      \
+                       int64_t cap = INT64_MAX; /* no workspace: the path never touches one */                     \
+                       return kron3_entry<T>(transa, transb, transc, m_a, n_a, m_b, n_b, m_c, n_c, p.batch_count,  \
+                                             alpha, A, lda, lena, B, ldb, lenb, C, ldc, lenc,                      \
+                                             static_cast<const T*>(p.X), ldx, ldx2, ldxp, p.lenx, beta,            \
+                                             static_cast<T*>(p.Y), ldy, ldy2, ldyp, p.leny, nullptr, cap, ex, e,   \
+                                             el, dry);                                                             \
+                     });                                                                                           \
+  }
+KB_PARTS3(kb_skron3_parts, float)
+KB_PARTS3(kb_dkron3_parts, double)
 
 }  // extern "C"

@@ -1,0 +1,48 @@
+"""compute-sanitizer over one small call of every kernel family (-m gpu).
+
+SURVEY.md §5: the reference has no sanitizers (proj/CMakeLists.txt:1-52), but
+the sm_100a kernels double-buffer shared memory behind mbarriers and bulk
+(TMA) copies, so memcheck (out-of-bounds / misaligned accesses -- including
+the odd-n group spans, which must not read past the batch), racecheck
+(shared-memory hazards) and synccheck (barrier misuse) run over
+tools/sanitize/kb_sanitize.cpp: every square size n = 1..16 in fp32/fp64 for
+2-D (op_x N and T) and 3-D, the generic, scale, kron1, gemm_a and 3xTF32
+tensor-core kernels, on exactly-sized device buffers.
+"""
+import os
+import shutil
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DRIVER = os.path.join(ROOT, "build", "sanitize", "kb_sanitize")
+CS = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+def _run(tool, mode, timeout):
+    if not os.path.exists(DRIVER):
+        pytest.skip("build/sanitize/kb_sanitize not built (make sanitize)")
+    cmd = [CS, "--tool", tool, "--error-exitcode", "97", "--print-limit", "20"]
+    if tool == "racecheck":
+        cmd += ["--racecheck-report", "all"]
+    cmd += [DRIVER, mode]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+    assert "0 failures" in out, out[-4000:]
+    return out
+
+
+def test_memcheck_every_kernel_family():
+    _run("memcheck", "full", 1500)
+
+
+def test_racecheck_kernel_families():
+    _run("racecheck", "quick", 1500)
+
+
+def test_synccheck_kernel_families():
+    _run("synccheck", "quick", 900)

@@ -66,6 +66,69 @@ def _worker(rank, world, port, batch, out_q):
     dist.destroy_process_group()
 
 
+def _gpu_worker(rank, world, port, batch, out_q):
+    """One process per 'GPU' (both on cuda:0 here): the rank's contiguous shard
+    runs through the PRODUCT (kb.kron3, device-resident, the bench's layout),
+    the host barrier / result exchange is gloo -- no NCCL, no data-path
+    collective."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_1304_7054_b200 as kb
+    from oracle.oracle import Oracle
+
+    torch.cuda.set_device(0)
+    o = Oracle()
+    n = 16
+    e = n ** 3
+    a, b, c, x, y = o.generate_batch(np.float64, 4, n, True, batch)
+    p0, p1 = shard_range(rank, world, batch)
+    cnt = p1 - p0
+    X = torch.from_numpy(x[p0 * e:p1 * e].copy()).cuda()
+    Y = torch.zeros(cnt * e, dtype=torch.float64, device="cuda")
+    pr = kb.KronProblem3D(m_a=n, n_a=n, m_b=n, n_b=n, m_c=n, n_c=n)
+    if cnt:
+        kb.kron3(pr, MatrixView(a, n, n, n), MatrixView(b, n, n, n), MatrixView(c, n, n, n),
+                 BatchView(kb.Array3View(X, n, n, n, n, n * n), cnt, e),
+                 BatchView(kb.Array3View(Y, n, n, n, n, n * n), cnt, e), kb.Workspace(None, cnt * e))
+    dist.barrier()  # host barrier between the shards
+    per = -(-batch // world)
+    buf = torch.zeros(per * e, dtype=torch.float64)
+    buf[:cnt * e] = Y.cpu()
+    parts = [torch.zeros(per * e, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(parts, buf)
+    if rank == 0:
+        full = np.concatenate([parts[r][:(shard_range(r, world, batch)[1] - shard_range(r, world, batch)[0]) * e]
+                               .numpy() for r in range(world)])
+        ref = np.zeros(batch * e)
+        o.kron3("N", "N", "N", n, n, n, n, n, n, batch, 1.0, a, n, b, n, c, n, x, n, n * n, e, 0.0, ref, n, n * n, e)
+        out_q.put(bool(np.array_equal(full.view(np.uint64), ref.view(np.uint64))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run_world(target, batch, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, batch, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert q.get(timeout=5) is True
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batch", [777, 1])
+def test_gloo_world2_library_shards_gpu(batch):
+    _run_world(_gpu_worker, batch)
+
+
 @pytest.mark.parametrize("batch", [1001, 2])
 def test_gloo_world2_shards_are_bit_identical(batch):
     ctx = mp.get_context("spawn")
