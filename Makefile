@@ -14,11 +14,11 @@ CSRC      := $(PKG)/csrc
 OBJDIR    := build/obj
 SRCS      := $(CSRC)/kb_runtime.cu $(CSRC)/kb_devmgr.cu $(CSRC)/kb_generic.cu $(CSRC)/kb_fast_switch.cu $(CSRC)/kb_tc.cu $(CSRC)/kb_blas.cu \
              $(sort $(wildcard $(CSRC)/kb_sz*.cu))
-OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
+OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS)) $(OBJDIR)/kb_hostcopy.o
 HDRS      := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/kronbatch_b200.h
 LIB       := $(PKG)/libkronbatch_b200.so
 
-.PHONY: all lib oracle cpptest kronbench sanitize clean
+.PHONY: all lib oracle accept cpptest kronbench sanitize clean
 all: lib oracle
 
 lib: $(LIB)
@@ -27,11 +27,19 @@ $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
+$(OBJDIR)/kb_hostcopy.o: $(CSRC)/kb_hostcopy.cpp
+	@mkdir -p $(OBJDIR)
+	$(CXX_HOST) -O3 -std=c++17 -fPIC -c $< -o $@
+
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
 
 oracle:
 	$(MAKE) -s -C oracle all
+
+# the reference's own acceptance binary against the drop-in headers (test infrastructure)
+accept: $(LIB)
+	$(MAKE) -s -C oracle accept
 
 CPPTESTS := build/cpptest/test_dropin
 cpptest: $(CPPTESTS)

@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
 #pragma unroll
       for (int m = 0; m < N; ++m) {
         T t[R];
-        lds_n<R, K::VR>(t, tr + m * N);
+        lds_rows<R, K::VR>(t, tr + m * N, two);
 #pragma unroll
         for (int j = 0; j < N; ++j) axpy_rows<R>(acc[j], t, kc.w[j * N + m]);
       }

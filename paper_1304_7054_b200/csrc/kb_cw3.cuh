@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
         for (int j = 0; j < N; ++j) pl[j * N] = acc[j];
       }
     } else if (m2_ok) {
+      const bool two2 = N % 2 == 0 || q2 * R + 1 < N;
       T* pl = buf + (P2 / N) * ITEM + (P2 % N) * PS + q2 * R;
       T acc[N][R];
 #pragma unroll
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
 #pragma unroll kCwUnroll
       for (int m = 0; m < N; ++m) {
         T t[R];
-        lds_n<R, K::VR>(t, pl + m * N);
+        lds_rows<R, K::VR>(t, pl + m * N, two2);
 #pragma unroll
         for (int j = 0; j < N; ++j) axpy_rows<R>(acc[j], t, kc.bt[m * kc.LD + j]);
       }
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
           *reinterpret_cast<double2*>(pl + j * N) = make_double2(acc[j][0], acc[j][1]);
         else {
           pl[j * N] = acc[j][0];
-          if (N % 2 == 0 || q2 * R + 1 < N) pl[j * N + 1] = acc[j][1];  // odd n: last task owns one row
+          if (two2) pl[j * N + 1] = acc[j][1];  // odd n: last task owns one row
         }
       }
     }
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
 #pragma unroll kCwUnroll
       for (int n = 0; n < N; ++n) {
         T f[R];
-        lds_n<R, K::VR>(f, fb + n * PS);
+        lds_rows<R, K::VR>(f, fb + n * PS, two);
 #pragma unroll
         for (int k = 0; k < N; ++k) axpy_rows<R>(acc[k], f, kc.ct[n * kc.LD + k]);
       }

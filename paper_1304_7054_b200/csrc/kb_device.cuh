@@ -178,6 +178,19 @@ __device__ __forceinline__ void lds_n(T* dst, const T* src) {
   for (int i = 0; i < n; i += VW) lds_vec<VW>(dst + i, src + i);
 }
 
+// R consecutive rows of a row block; odd n: the last block of a column has a
+// single row (two == false) and must not touch the next column's first element
+// (another thread's, which may be written concurrently in place).
+template <int R, int VW, typename T>
+__device__ __forceinline__ void lds_rows(T* dst, const T* src, bool two) {
+  if constexpr (R == 2 && VW == 1) {
+    dst[0] = src[0];
+    dst[1] = two ? src[1] : T(0);
+  } else {
+    lds_n<R, VW>(dst, src);
+  }
+}
+
 // Store n consecutive elements to global memory with vector width VW.
 template <int n, int VW, typename T>
 __device__ __forceinline__ void stg_n(T* dst, const T* src) {

@@ -69,6 +69,11 @@ struct Lane {
   DevBuf scratch[kSlots];
   DevBuf xs[kSlots], ys[kSlots];                // device staging (host-resident X / Y)
   HostBuf hx[kSlots], hy[kSlots];               // pinned bounce buffers (pageable X / Y)
+  bool used = false;  // this checkout handed a device buffer (constants / scratch) to a kernel
+  DevBuf& use(DevBuf& b) {
+    used = true;
+    return b;
+  }
   size_t bytes_held() const;
 };
 
@@ -77,8 +82,12 @@ struct Lane {
 // being captured into a CUDA graph -- no event queries / waits (illegal
 // during capture); the graph's own dependencies order its pooled-buffer uses.
 Lane* acquire_lane(int dev, bool capturing = false);
-// Return a lane. If `async_stream` is non-null the lane's buffers may still be
-// read by work queued on that stream: an event is recorded there first.
+// Return a lane. If `async_stream` is non-null and the call handed one of the
+// lane's device buffers to a kernel (Lane::use), that kernel may still be
+// reading it: an event is recorded on the stream first, and the lane is only
+// handed out again once the event has completed. (The square fast paths take
+// their constants as kernel parameters and use no lane buffer, so their
+// asynchronous calls return the lane immediately reusable.)
 void release_lane(Lane* l, cudaStream_t async_stream);
 
 // RAII checkout.

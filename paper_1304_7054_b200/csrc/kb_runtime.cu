@@ -226,7 +226,7 @@ void run2_device(const K2<T>& k, const T* A, const T* B, const T* ha, const T* h
   i64 scratch_elems = 0;
   if ((size_t)per * sizeof(T) > 48 * 1024) {
     scratch_elems = per * grid;
-    scratch = static_cast<T*>(r.scratch[slot].get(sizeof(T) * (size_t)scratch_elems));
+    scratch = static_cast<T*>(r.use(r.scratch[slot]).get(sizeof(T) * (size_t)scratch_elems));
   }
   cuda_check(kb::launch_kron2_generic<T>(p, scratch, scratch_elems, grid, s), "kron2");
   count_launch("kron2_generic");
@@ -447,7 +447,7 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
       auto upload = [&](Lane& r, cudaStream_t s) {
         if (Ad) return;
         const i64 fa = fp_matrix(ac, lda), fb = fp_matrix(bc, ldb);
-        T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + fb + 64)));
+        T* cs = static_cast<T*>(r.use(r.consts).get(sizeof(T) * (size_t)(fa + fb + 64)));
         Ad = const_on_device(A, fa, r.device, cs, s);
         Bd = const_on_device(B, fb, r.device, cs + fa + 32, s);
       };
@@ -539,7 +539,7 @@ int kron1_entry(char ta, i64 m_a, i64 n_a, i64 batch, T alpha, const T* A, i64 l
               ha = resolve_sq(fetch_host(A, fa, s), lda, is_t(ta), (int)m_a, false, T(1), false);
               return;
             }
-            T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + 32)));
+            T* cs = static_cast<T*>(r.use(r.consts).get(sizeof(T) * (size_t)(fa + 32)));
             Ad = const_on_device(A, fa, r.device, cs, s);
           },
           [&](const void* xd, void* yd, i64 n, Lane& r, cudaStream_t s, int) {
@@ -617,7 +617,7 @@ int gemm_a_entry(char ta, char tb, i64 m, i64 n, i64 k, i64 batch, T alpha, cons
               hw = resolve_sq(fetch_host(B, fb, s), ldb, is_t(tb), (int)m, false, alpha, !is_t(ta));
               return;
             }
-            T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fb + 32)));
+            T* cs = static_cast<T*>(r.use(r.consts).get(sizeof(T) * (size_t)(fb + 32)));
             Bd = const_on_device(B, fb, r.device, cs, s);
           },
           [&](const void* ad, void* cd, i64 nb, Lane& r, cudaStream_t s, int) {
@@ -723,7 +723,7 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
       auto upload = [&]() {  // A/B/C on the device (in place when already resident)
         if (Ad) return;
         Lane& r = *rp;
-        T* cs = static_cast<T*>(r.consts.get(sizeof(T) * (size_t)(fa + fb + fc + 96)));
+        T* cs = static_cast<T*>(r.use(r.consts).get(sizeof(T) * (size_t)(fa + fb + fc + 96)));
         Ad = const_on_device(A, fa, r.device, cs, up_stream);
         Bd = const_on_device(B, fb, r.device, cs + fa + 32, up_stream);
         Cd = const_on_device(Cm, fc, r.device, cs + fa + fb + 64, up_stream);
@@ -795,7 +795,7 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                   i64 scratch_elems = 0;
                   if ((size_t)per * sizeof(T) > 48 * 1024) {
                     scratch_elems = per * grid;
-                    scratch = static_cast<T*>(r.scratch[slot].get(sizeof(T) * (size_t)scratch_elems));
+                    scratch = static_cast<T*>(r.use(r.scratch[slot]).get(sizeof(T) * (size_t)scratch_elems));
                   }
                   cuda_check(kb::launch_kron3_generic<T>(p, scratch, scratch_elems, grid, s), "kron3");
                   count_launch("kron3_generic");

@@ -48,10 +48,20 @@ def test_verify_only_all_sizes():
 @pytest.mark.gpu
 @pytest.mark.parametrize("resident", [False, True])
 def test_csv_schema(resident):
-    args = ["--format", "csv", "--sizes", "10,16", "--batch", "2000", "--reps", "3", "--beta", "0.5"]
+    args = ["--format", "csv", "--sizes", "10,16", "--batch", "2000", "--reps", "3", "--beta", "0.5", "--b200-columns"]
     r = run(*args, *(["--resident"] if resident else []))
     assert r.returncode == 0, r.stderr
     rows = list(csv.DictReader(io.StringIO(r.stdout)))
     assert list(rows[0].keys())[:7] == ["size", "precision", "dims", "batch", "seconds", "gflops", "verified"]
     assert len(rows) == 8 and all(x["verified"] == "true" and float(x["gflops"]) > 0 for x in rows)
     assert all(x["mode"] == ("resident" if resident else "host") for x in rows)
+
+
+@needs_exe
+@pytest.mark.gpu
+def test_csv_reference_schema_by_default():
+    r = run("--format", "csv", "--sizes", "2,3", "--batch", "100", "--reps", "1")
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    assert lines[0] == "size,precision,dims,batch,seconds,gflops,verified"  # bench_support.cpp:346-352
+    assert len(lines) == 9 and all(len(l.split(",")) == 7 for l in lines)
