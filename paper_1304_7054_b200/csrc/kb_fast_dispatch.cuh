@@ -218,56 +218,9 @@ static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, 
   return cudaGetLastError();
 }
 
-// n = 16 warp-plane column-wise kernel (kb_cw3.cuh), S stages.
-template <typename T, int S, bool EARLY>
-static cudaError_t launch3cwp(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
-                              cudaStream_t s) {
-  constexpr int N = 16;
-  using K = Cwp3<T, S, EARLY>;
-  if (p.ldx != N || p.ldx2 != (long long)N * N || (p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))
-    return cudaErrorNotSupported;
-  if (p.ldy % 2 || p.ldy2 % 2 || p.sy % 2 || !aligned<T>(p.Y, 2)) return cudaErrorNotSupported;
-  auto kern = p.beta_mode == kBetaZero ? kron3_cwp_kernel<T, S, EARLY, true> : kron3_cwp_kernel<T, S, EARLY, false>;
-  const size_t smem = K::smem_bytes();
-  const int occ = occupancy_for(kern, K::THREADS, smem);
-  if (occ <= 0) return cudaErrorNotSupported;
-  const long long ntiles = p.batch;
-  const int grid = (int)(ntiles < (long long)sm_count * occ ? ntiles : (long long)sm_count * occ);
-  SqConstsCw3<T, N> kc;
-  for (int i = 0; i < N; ++i)
-    for (int j = 0; j < N; ++j) {
-      kc.a[i + j * kc.LD] = ha[i + j * N];
-      kc.bt[j * kc.LD + i] = hb[i * N + j];
-      kc.ct[j * kc.LD + i] = hc[i * N + j];
-    }
-  kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
-  return cudaGetLastError();
-}
-
-template <typename T>
-static cudaError_t launch3cwpp(const Kron3Params<T>& p, const T* ha, const T* hb, const T* hc, int sm_count,
-                               cudaStream_t s) {
-  constexpr int N = 16;
-  using K = Cwpp3<T>;
-  if (p.ldx != N || p.ldx2 != (long long)N * N || (p.sx * (long long)sizeof(T)) % 16 || !aligned<T>(p.X, 16 / sizeof(T)))
-    return cudaErrorNotSupported;
-  if (p.ldy % 2 || p.ldy2 % 2 || p.sy % 2 || !aligned<T>(p.Y, 2)) return cudaErrorNotSupported;
-  auto kern = kron3_cwpp_kernel<T>;
-  const size_t smem = K::smem_bytes();
-  const int occ = occupancy_for(kern, K::THREADS, smem);
-  if (occ <= 0) return cudaErrorNotSupported;
-  const long long ntiles = p.batch;
-  const int grid = (int)(ntiles < (long long)sm_count * occ ? ntiles : (long long)sm_count * occ);
-  SqConstsCw3<T, N> kc;
-  for (int i = 0; i < N; ++i)
-    for (int j = 0; j < N; ++j) {
-      kc.a[i + j * kc.LD] = ha[i + j * N];
-      kc.bt[j * kc.LD + i] = hb[i * N + j];
-      kc.ct[j * kc.LD + i] = hc[i * N + j];
-    }
-  kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
-  return cudaGetLastError();
-}
+#ifdef KB_SWEEP_VARIANTS  // n = 16 warp-plane experiments, kept out of the product tree
+#include "../../tools/variants/kb_cw3_variants.cuh"
+#endif
 
 // Tiny-entry 3-D kernel (kb_tiny3.cuh), n <= 4, tight entries.
 template <typename T, int N>
