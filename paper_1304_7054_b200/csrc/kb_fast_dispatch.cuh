@@ -219,7 +219,9 @@ static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, 
 }
 
 #ifdef KB_SWEEP_VARIANTS  // n = 16 warp-plane experiments, kept out of the product tree
+}  // namespace kb
 #include "../../tools/variants/kb_cw3_variants.cuh"
+namespace kb {
 #endif
 
 // Tiny-entry 3-D kernel (kb_tiny3.cuh), n <= 4, tight entries.

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/kronbatch_b200.h"
 #include "kb_devmgr.h"
@@ -40,6 +41,15 @@ thread_local std::string t_last_path;
 
 using kbrt::Fail;
 using kbrt::cuda_check;
+
+// NVTX range (header-only NVTX3: a no-op unless a profiler is attached), so an
+// nsys / ncu timeline shows each call, its per-GPU slices and staged chunks.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 int report(const Fail& f, char* err, size_t errlen) {
   if (err && errlen) {
@@ -269,6 +279,7 @@ template <typename Prep, typename Compute>
 void run_slice(int dev, const void* X, void* Y, i64 p0, i64 p1, const StageSpec& sp, bool x_dev, bool y_dev,
                cudaStream_t user_stream, bool sync, Prep&& prep, Compute&& compute) {
   if (p1 <= p0) return;
+  Nvtx range("kb slice");
   DeviceGuard g(dev);
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (user_stream && cudaStreamIsCapturing(user_stream, &cap) != cudaSuccess) {
@@ -322,6 +333,7 @@ void run_slice(int dev, const void* X, void* Y, i64 p0, i64 p1, const StageSpec&
   std::vector<kbrt::CopyJob> jobs;
   i64 c = 0;
   for (i64 q0 = p0; q0 < p1; q0 += chunk, ++c) {
+    Nvtx chunk_range("kb staged chunk");
     const i64 q1 = std::min(p1, q0 + chunk), n = q1 - q0;
     const int slot = (int)(c % nslots);
     cudaStream_t s = r.slot_stream[slot];
@@ -408,6 +420,7 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                 i64 lda, i64 lena, const T* B, i64 ldb, i64 lenb, const T* X, i64 ldx, i64 ldxp, i64 lenx, T beta,
                 T* Y, i64 ldy, i64 ldyp, i64 leny, const kb_exec* exec, char* err, size_t errlen,
                 bool dry = false) {
+  Nvtx range("kb call");
   t_last_path.clear();
   try {
     check_op("kron2: A", ta);
@@ -661,6 +674,7 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                 i64 leny, T* work, i64 work_cap, const kb_exec* exec, char* err, size_t errlen,
                 bool dry = false) {
   (void)work;
+  Nvtx range("kb call");
   t_last_path.clear();
   try {
     check_op("kron3: A", ta);

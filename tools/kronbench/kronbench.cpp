@@ -10,6 +10,7 @@
 //   gbs,hbm_frac,roof_frac,mode
 // Extra flags (not in the reference):
 //   --b200-columns   append gbs,hbm_frac,roof_frac,mode to the CSV
+//   --mb-per-size M  batch per size = ceil(M MiB / entry bytes of X) instead of --batch
 //   --resident       X/Y live in device memory, timed with CUDA events on the
 //                    library stream (kernel throughput); default is the
 //                    reference's host-buffer call (end to end, PCIe staged)
@@ -54,6 +55,7 @@ struct Config {
   std::uint64_t seed = 1;
   bool csv = false, verify_only = false, resident = false, b200_cols = false;
   int gpus = 1;
+  long long bytes_per_size = 0;
   double hbm_gbs = 6539.9;
   std::string out_path;
 };
@@ -322,7 +324,8 @@ std::string fmt6(double v) {  // 6 significant digits, like printf %g
 void usage() {
   std::cerr << "usage: kronbench [--sizes lo..hi|a,b,...] [--precision single|double|both] [--dims 2d|3d|both]\n"
                "                 [--batch N] [--reps R] [--alpha A] [--beta B] [--seed S] [--format table|csv]\n"
-               "                 [--out FILE] [--verify-only] [--resident] [--gpus N] [--hbm-gbs G] [--b200-columns]\n";
+               "                 [--out FILE] [--verify-only] [--resident] [--gpus N] [--hbm-gbs G] [--b200-columns]\n"
+               "                 [--mb-per-size M]\n";
 }
 
 }  // namespace
@@ -350,6 +353,7 @@ int main(int argc, char** argv) {
       else if (a == "--verify-only") cfg.verify_only = true;
       else if (a == "--resident") cfg.resident = true;
       else if (a == "--b200-columns") cfg.b200_cols = true;
+      else if (a == "--mb-per-size") cfg.bytes_per_size = std::stoll(val()) << 20;
       else if (a == "--gpus") cfg.gpus = std::stoi(val());
       else if (a == "--hbm-gbs") cfg.hbm_gbs = std::stod(val());
       else if (a == "-h" || a == "--help") {
@@ -385,7 +389,11 @@ int main(int argc, char** argv) {
         if ((p == Prec::Single && !cfg.single) || (p == Prec::Double && !cfg.dbl)) continue;
         for (Dims dd : {Dims::D2, Dims::D3}) {
           if ((dd == Dims::D2 && !cfg.d2) || (dd == Dims::D3 && !cfg.d3)) continue;
-          const index_t batch = cfg.batch > 0 ? cfg.batch : (p == Prec::Single ? 100000 : 50000);
+          index_t batch = cfg.batch > 0 ? cfg.batch : (p == Prec::Single ? 100000 : 50000);
+          if (cfg.bytes_per_size > 0) {  // batch sized so X alone is bytes_per_size (BASELINE configs[4] sweep)
+            const index_t entry = (dd == Dims::D2 ? (index_t)m * m : (index_t)m * m * m) * (p == Prec::Single ? 4 : 8);
+            batch = (cfg.bytes_per_size + entry - 1) / entry;
+          }
           recs.push_back(p == Prec::Single ? run_one<float>(cfg, m, dd, batch, out)
                                            : run_one<double>(cfg, m, dd, batch, out));
         }
