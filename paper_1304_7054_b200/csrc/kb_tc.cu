@@ -62,6 +62,7 @@ template <int WGS>
 struct Smem {
   alignas(128) unsigned char ct[3][2][CT_BYTES];  // [mode][hi, lo] (no-swizzle operands: 16-byte alignment suffices)
   alignas(16) float slice[WGS][SLICE];
+  alignas(128) float ystage[WGS][N * N * N];  // Y staging for the bulk store (tight Y, beta = 0)
   unsigned long long dbar[WGS];
   unsigned tmem_base;
 };
@@ -152,6 +153,16 @@ __device__ __forceinline__ unsigned long long smem_desc(const void* p, unsigned 
          ((unsigned long long)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // version 1, SWIZZLE_NONE
 }
 
+// shared -> global bulk copy (TMA engine), tracked by this thread's bulk groups
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // element (n, k) of a 16 x 16 constant operand tile
@@ -210,6 +221,8 @@ __global__ void __launch_bounds__(WGS * 128, 1)
     for (int h = 0; h < 2; ++h) bd[md][h] = smem_desc(sm.ct[md][h], 256, 128);
   float* slice = sm.slice[g];
   const int bar_id = 1 + g;
+  const bool ybulk = beta_mode == kBetaZero && ldy == N && ldy2 == N * N && sy % 4 == 0 &&
+                     (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
 
   // entries of this group: e = first + k * stride
   const long long stride = (long long)gridDim.x * WGS;
@@ -344,6 +357,7 @@ __global__ void __launch_bounds__(WGS * 128, 1)
       split_store(v[0], 0);
       split_store(v[1], 1);
     }
+    if (ybulk && leader) bulk_wait_read();  // the previous entry's Y has left the staging buffer
     sync_group();  // (also: every exchange read is done before the slice is reused)
     TC_STAMP(5);
     issue_mode(2);
@@ -357,21 +371,35 @@ __global__ void __launch_bounds__(WGS * 128, 1)
       tmem_ld16(tbase + 80, d[1]);
       tmem_ld_wait();
       TC_STAMP(12);
-      float* yp = Y + e * sy + (long long)(L >> 4) * ldy + (L & 15);
+      if (ybulk) {
+        // tight Y, beta = 0: stage the entry in the group's slice in Y's own
+        // layout (k*256 + 16 j + i: per k a warp writes 32 consecutive words)
+        // and let one thread's bulk copy (TMA engine) write the 16 KB to HBM
+        float* st = sm.ystage[g] + 16 * (L >> 4) + (L & 15);
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        float* yt = yp + (long long)(8 * t) * ldy;
-        if (beta_mode == kBetaZero) {
-#ifdef KB_TC_EXP_NO_Y  // timing experiment only: skip the Y stores
-          if (d[t][0] == 12345.f)
-#endif
+        for (int t = 0; t < 2; ++t)
 #pragma unroll
-          for (int k = 0; k < 16; ++k) __stcs(yt + k * ldy2, d[t][k]);
-        } else {
+          for (int k = 0; k < 16; ++k) st[t * 128 + k * 256] = d[t][k];
+        fence_proxy_async();
+        named_bar(bar_id, 128);
+        if (leader) {
+          bulk_s2g(Y + e * sy, sm.ystage[g], N * N * N * 4);
+          bulk_commit();
+        }
+      } else {
+        float* yp = Y + e * sy + (long long)(L >> 4) * ldy + (L & 15);
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const float y0 = yt[k * ldy2];
-            yt[k * ldy2] = d[t][k] + (beta_mode == kBetaOne ? y0 : beta * y0);
+        for (int t = 0; t < 2; ++t) {
+          float* yt = yp + (long long)(8 * t) * ldy;
+          if (beta_mode == kBetaZero) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) __stcs(yt + k * ldy2, d[t][k]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const float y0 = yt[k * ldy2];
+              yt[k * ldy2] = d[t][k] + (beta_mode == kBetaOne ? y0 : beta * y0);
+            }
           }
         }
       }
@@ -380,6 +408,7 @@ __global__ void __launch_bounds__(WGS * 128, 1)
     tc_fence_before();  // D reads done before the next entry's MMAs overwrite it (ordered by sync_group)
   }
 
+  if (ybulk && leader) bulk_wait_all();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

@@ -3,12 +3,14 @@
 // KronProblem structs, exceptions), running on the B200 library. Exit status
 // 0 = all checks passed. Run by tests/test_gpu_cpp.py (-m gpu).
 #include <cmath>
+#include <cstring>
 #include <cstdio>
 #include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include <kronbatch/b200_parts.hpp>
 #include <kronbatch/kronbatch.hpp>
 
 using namespace kronbatch;
@@ -187,7 +189,34 @@ void test_kron1_gemm_a(int m, int batch) {
   CHECK(threw);
 }
 
+// kb_?kron2_parts through the C++ wrapper: a host batch split into 3 ragged
+// parts (all on device 0 here) == one kron2 over the whole batch, bit for bit.
+template <typename T>
+void test_parts(int m, int batch) {
+  std::mt19937_64 g(99 + m);
+  auto a = rnd<T>(m * m, g), b = rnd<T>(m * m, g), x = rnd<T>(m * m * batch, g);
+  std::vector<T> y1(m * m * batch, T(0)), y2(m * m * batch, T(0));
+  KronProblem2D<T> pr;
+  pr.m_a = pr.n_a = pr.m_b = pr.n_b = m;
+  const index_t e = (index_t)m * m;
+  MatrixView<const T> va(std::span<const T>(a), m, m, m), vb(std::span<const T>(b), m, m, m);
+  kron2<T>(pr, va, vb, BatchView<MatrixView<const T>>(MatrixView<const T>(std::span<const T>(x), m, m, m), batch, e),
+           BatchView<MatrixView<T>>(MatrixView<T>(std::span<T>(y1), m, m, m), batch, e));
+  const int cuts[4] = {0, batch / 3, batch / 3 + 1, batch};
+  std::vector<b200::Part2<T>> parts;
+  for (int i = 0; i < 3; ++i) {
+    const index_t p0 = cuts[i], n = cuts[i + 1] - cuts[i];
+    parts.push_back(b200::Part2<T>{
+        0, BatchView<MatrixView<const T>>(MatrixView<const T>(std::span<const T>(x).subspan(p0 * e, n * e), m, m, m), n, e),
+        BatchView<MatrixView<T>>(MatrixView<T>(std::span<T>(y2).subspan(p0 * e, n * e), m, m, m), n, e), nullptr});
+  }
+  b200::kron2_parts<T>(pr, va, vb, std::span<const b200::Part2<T>>(parts));
+  CHECK(std::memcmp(y1.data(), y2.data(), sizeof(T) * y1.size()) == 0);
+}
+
 int main() {
+  test_parts<float>(16, 1001);
+  test_parts<double>(9, 333);
   for (int m : {1, 5, 16, 24}) {
     test_kron1_gemm_a<float>(m, 500);
     test_kron1_gemm_a<double>(m, 200);
