@@ -64,7 +64,7 @@ void HostBuf::release() {
 
 size_t Lane::bytes_held() const {
   size_t b = consts.cap;
-  for (int i = 0; i < kSlots; ++i) b += scratch[i].cap + xs[i].cap + ys[i].cap;
+  for (int i = 0; i < kSlots; ++i) b += scratch[i].cap + xs[i].cap + ys[i].cap + pk[0][i].cap + pk[1][i].cap;
   return b;
 }
 
@@ -142,6 +142,8 @@ void destroy_lane(Lane* l) {
     l->ys[i].release();
     l->hx[i].release();
     l->hy[i].release();
+    l->pk[0][i].release();
+    l->pk[1][i].release();
     cudaStreamDestroy(l->slot_stream[i]);
   }
   cudaStreamDestroy(l->stream);

@@ -141,6 +141,43 @@ cudaError_t launch_scale(T* Y, long long batch, long long d1, long long d2, long
   return cudaGetLastError();
 }
 
+// Strided batch copy: entry p, element (i, j, k) of d1 x d2 x d3 from
+// src[p*s_stride + i + j*s_ld + k*s_ld2] to dst[p*d_stride + i + j*d_ld + k*d_ld2].
+// Thread per element in (i fastest) order: the tight side is fully coalesced,
+// the strided side reads / writes runs of d1 contiguous elements. Only entry
+// elements are touched (padding of either layout is never read or written).
+template <typename T>
+__global__ void __launch_bounds__(256) repack_kernel(const T* __restrict__ src, long long s_ld, long long s_ld2,
+                                                     long long s_stride, T* __restrict__ dst, long long d_ld,
+                                                     long long d_ld2, long long d_stride, int d1, int d2, int d3,
+                                                     long long total) {
+  const long long per = (long long)d1 * d2 * d3;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long p = t / per;
+    const int r = (int)(t - p * per);
+    const int i = r % d1, jk = r / d1, j = jk % d2, k = jk / d2;
+    dst[p * d_stride + i + j * d_ld + k * d_ld2] = src[p * s_stride + i + j * s_ld + k * s_ld2];
+  }
+}
+
+template <typename T>
+cudaError_t launch_repack(const T* src, long long s_ld, long long s_ld2, long long s_stride, T* dst, long long d_ld,
+                          long long d_ld2, long long d_stride, int d1, int d2, int d3, long long batch, int sm_count,
+                          cudaStream_t s) {
+  const long long total = batch * d1 * d2 * d3;
+  if (total <= 0) return cudaSuccess;
+  const long long want = (total + 255) / 256, cap = (long long)sm_count * 16;
+  repack_kernel<T><<<(int)(want < cap ? want : cap), 256, 0, s>>>(src, s_ld, s_ld2, s_stride, dst, d_ld, d_ld2,
+                                                                    d_stride, d1, d2, d3, total);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_repack<float>(const float*, long long, long long, long long, float*, long long, long long,
+                                          long long, int, int, int, long long, int, cudaStream_t);
+template cudaError_t launch_repack<double>(const double*, long long, long long, long long, double*, long long,
+                                           long long, long long, int, int, int, long long, int, cudaStream_t);
+
 template cudaError_t launch_kron2_generic<float>(const Kron2Params<float>&, float*, long long, int, cudaStream_t);
 template cudaError_t launch_kron2_generic<double>(const Kron2Params<double>&, double*, long long, int, cudaStream_t);
 template cudaError_t launch_kron3_generic<float>(const Kron3Params<float>&, float*, long long, int, cudaStream_t);

@@ -22,6 +22,13 @@ template <typename T>
 cudaError_t launch_scale(T* Y, long long batch, long long d1, long long d2, long long d3, long long ld,
                          long long ld2, long long sy, int beta_mode, T beta, int grid, cudaStream_t s);
 
+// Strided batch copy (padded <-> tight entry layouts) for the square
+// fast paths on padded / strided callers: entry elements only, padding untouched.
+template <typename T>
+cudaError_t launch_repack(const T* src, long long s_ld, long long s_ld2, long long s_stride, T* dst, long long d_ld,
+                          long long d_ld2, long long d_stride, int d1, int d2, int d3, long long batch, int sm_count,
+                          cudaStream_t s);
+
 // Square n <= 16 register-blocked kernels. Return cudaErrorNotSupported
 // (without launching) when the layout does not meet the fast-path
 // preconditions (tight entries, vector alignment); the caller then uses the

@@ -210,6 +210,35 @@ struct K2 {
   T* Y; i64 ldy, sy, fpy;
 };
 
+// Square n <= 16 on a padded / strided layout the fast kernels cannot stream
+// (ld != n, ragged entry strides): repack each chunk into tight lane buffers,
+// run the fast kernel there, repack Y back (entry elements only: padding is
+// never written). Chunks of <= 32 MiB per side stay resident in the 126 MB L2
+// between the three kernels, so HBM mostly sees X once and Y once; same
+// per-element arithmetic as the generic kernel (bit-identical).
+constexpr i64 kRepackBytes = i64(32) << 20;
+
+template <typename T, typename Fast>
+void run_repacked(int dims, int N, const T* X, i64 ldx, i64 ldx2, i64 sx, T* Y, i64 ldy, i64 ldy2, i64 sy,
+                  bool y_in, i64 n, Lane& r, cudaStream_t s, int slot, Fast&& fast) {
+  const i64 e = dims == 3 ? (i64)N * N * N : (i64)N * N;
+  const int d3 = dims == 3 ? N : 1;
+  const i64 chunk = std::max<i64>(1, std::min<i64>(n, kRepackBytes / (e * (i64)sizeof(T))));
+  T* xt = static_cast<T*>(r.use(r.pk[0][slot]).get(sizeof(T) * (size_t)(chunk * e)));
+  T* yt = static_cast<T*>(r.use(r.pk[1][slot]).get(sizeof(T) * (size_t)(chunk * e)));
+  for (i64 q0 = 0; q0 < n; q0 += chunk) {
+    const i64 c = std::min(chunk, n - q0);
+    cuda_check(kb::launch_repack<T>(X + q0 * sx, ldx, ldx2, sx, xt, N, (i64)N * N, e, N, N, d3, c, r.sm_count, s),
+               "repack X");
+    if (y_in)
+      cuda_check(kb::launch_repack<T>(Y + q0 * sy, ldy, ldy2, sy, yt, N, (i64)N * N, e, N, N, d3, c, r.sm_count, s),
+                 "repack Y");
+    cuda_check(fast(xt, yt, c), "repacked fast kernel");
+    cuda_check(kb::launch_repack<T>(yt, N, (i64)N * N, e, Y + q0 * sy, ldy, ldy2, sy, N, N, d3, c, r.sm_count, s),
+               "unpack Y");
+  }
+}
+
 // Launch the compute for entries [0, n) of device-resident X/Y views.
 template <typename T, typename Upload>
 void run2_device(const K2<T>& k, const T* A, const T* B, const T* ha, const T* hw, const T* X, T* Y, i64 n,
@@ -229,6 +258,17 @@ void run2_device(const K2<T>& k, const T* A, const T* B, const T* ha, const T* h
   }
   if (e != cudaErrorNotSupported) cuda_check(e, "kron2");
   cudaGetLastError();
+  if (ha) {  // square n <= 16, layout the fast kernels cannot stream: repack through tight buffers
+    run_repacked<T>(2, (int)k.m_a, X, k.ldx, 0, k.sx, Y, k.ldy, 0, k.sy, p.beta_mode != kb::kBetaZero, n, r, s, slot,
+                    [&](const T* xt, T* yt, i64 c) {
+                      Kron2Params<T> q = p;
+                      q.X = xt, q.Y = yt, q.ldx = k.m_a, q.sx = k.m_a * k.m_a, q.ldy = k.m_a, q.sy = k.m_a * k.m_a;
+                      q.batch = c;
+                      return kb::launch_kron2_fast<T>(q, ha, hw, r.sm_count, s);
+                    });
+    count_launch("kron2_repacked");
+    return;
+  }
   if (!p.A) upload(s, p.A, p.B);  // square call the fast path declined: device constants now
   const int grid = (int)std::min<i64>(n, (i64)r.sm_count * 8);
   const i64 per = k.m_a * k.n_b;
@@ -795,6 +835,21 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                   }
                   if (e != cudaErrorNotSupported) cuda_check(e, "kron3");
                   cudaGetLastError();
+                  if (square_fast) {  // padded / strided square layout: repack through tight buffers
+                    const int N = (int)m_a;
+                    run_repacked<T>(3, N, static_cast<const T*>(xd), ldx, ldx2, ldxp, static_cast<T*>(yd), ldy, ldy2,
+                                    ldyp, base.beta_mode != kb::kBetaZero, n, r, s, slot,
+                                    [&](const T* xt, T* yt, i64 c) {
+                                      Kron3Params<T> q = p;
+                                      q.X = xt, q.Y = yt, q.ldx = N, q.ldx2 = (i64)N * N, q.sx = (i64)N * N * N;
+                                      q.ldy = N, q.ldy2 = (i64)N * N, q.sy = (i64)N * N * N;
+                                      q.batch = c;
+                                      return kb::launch_kron3_fast<T>(q, ha.data(), hb.data(), hc.data(), r.sm_count,
+                                                                      s);
+                                    });
+                    count_launch("kron3_repacked");
+                    return;
+                  }
                   if (!Ad) {  // a square call the fast path declined (layout): constants now
                     up_stream = s;
                     upload();

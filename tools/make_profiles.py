@@ -87,7 +87,7 @@ def main(tag):
     if os.path.exists(lp):
         with open(os.path.join(out_dir, f"{tag}_launches.json"), "w") as f:
             json.dump({"command": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
-                                  "--clock-control none -c 400 python bench.py --steps 5 --warmup 3 --e2e-steps 1 --no-cpu --no-extra",
+                                  "--clock-control none -c 400 python bench.py --steps 5 --warmup 3 --e2e-steps 1 --no-cpu",
                        "kernels": launches(lp)}, f, indent=1)
     for b in ("bench.json", "bench_ref.json"):
         p = os.path.join(ROOT, "gpurun_out", b)
