@@ -74,7 +74,11 @@ struct Cw3 {
   // entries per tile: ~256 threads of mode-2/3 tasks (fp32, V0/V1), ~128
   // (fp64; fp32 V2: 4-warp CTAs, so each SM sub-partition interleaves warps
   // of six independent CTAs instead of three)
-  static constexpr int MAXT = ES == 4 && V != 2 ? 256 : 128;
+  static constexpr int MAXT = ES == 4 && V != 2 && V != 7 ? 256 : 128;
+  // V7: two independent groups of the V2 tile per CTA sharing a 3-stage ring
+  // (1.5 stages per group instead of 2: 8 groups = 32 warps per SM at n = 16
+  // fp32, where V2's 2-stage CTAs fit only 6 = 24 warps in shared memory)
+  static constexpr int G = V == 7 ? 2 : 1;
   // V2 / fp64: the smallest tile (entries) whose mode-2/3 tasks fill their
   // warps to >= 93 % (n = 10: 3 entries = 150 of 160 threads, not 2 = 100 of
   // 128), at most 384 threads; V0/V1: as many entries as fit MAXT threads
@@ -91,7 +95,7 @@ struct Cw3 {
       return 1;
     }
     if (V == 4) return 1;  // one entry per CTA: CTA barriers span only that entry's warps
-    if (ES == 4 && V != 2 && V != 3) return MAXT / (N * TPI) > 0 ? MAXT / (N * TPI) : 1;
+    if (ES == 4 && V != 2 && V != 3 && V != 7) return MAXT / (N * TPI) > 0 ? MAXT / (N * TPI) : 1;
     int best = 1, best_idle = 1 << 30;
     for (int it = 1; it * N * TPI <= 384 || it == 1; ++it) {
       const int t = it * N * TPI, w = (t + 31) / 32 * 32;
@@ -107,13 +111,15 @@ struct Cw3 {
   static constexpr int IT = pick_it();
   static constexpr int NP = IT * N;           // planes per tile
   static constexpr int NTASK = NP * TPI;      // mode-2 and mode-3 tasks per tile
-  static constexpr int THREADS = WP ? (NP + PPW - 1) / PPW * 32 : (NTASK + 31) / 32 * 32;
+  static constexpr int GT = WP ? (NP + PPW - 1) / PPW * 32 : (NTASK + 31) / 32 * 32;  // threads per group
+  static constexpr int THREADS = G * GT;
   static constexpr int NCOL = NP * N;         // mode-1 columns per tile
-  static constexpr int CA = WP ? (PPW * N + 31) / 32 : (NCOL + THREADS - 1) / THREADS;
-  static constexpr int STAGES = V == 1 ? 1 : 2;
+  static constexpr int CA = WP ? (PPW * N + 31) / 32 : (NCOL + GT - 1) / GT;
+  static constexpr int STAGES = V == 1 ? 1 : (V == 7 ? 3 : 2);
   // resident CTAs the register budget targets (~24 warps per SM)
   static constexpr int MINB_AUTO = 768 / ((IT * N * TPI + 31) / 32 * 32) > 0 ? 768 / ((IT * N * TPI + 31) / 32 * 32) : 1;
-  static constexpr int MINB = V == 6 ? (768 / THREADS > 0 ? 768 / THREADS : 1)
+  static constexpr int MINB = V == 7 ? 1024 / THREADS
+                             : V == 6 ? (768 / THREADS > 0 ? 768 / THREADS : 1)
                              : V == 4 ? MINB_AUTO
                              : V == 3 ? (ES == 4 ? 4 : 3)
                                      : (ES == 4 ? (V == 1 ? 4 : (V == 2 ? MINB_AUTO : 3)) : (V == 1 ? MINB_AUTO : 3));
@@ -181,7 +187,13 @@ struct Cw3 {
   static constexpr int PS = plane_stride();
   static constexpr int ITEM = N * PS;
   static constexpr int TILE = (IT * ITEM + SLACK + 16 / ES - 1) / (16 / ES) * (16 / ES);
-  static constexpr size_t smem_bytes() { return (size_t)ES * STAGES * TILE + 8 * STAGES; }
+  // mbarriers: one per stage, except V7 -- there a stage alternates between two
+  // barriers (tile k uses k % (2 S)), because a parity wait only tells
+  // adjacent phases apart and a group can reach tile k before the other
+  // group's load of tile k - S (same stage) has landed; with two barriers the
+  // previous phase of k's barrier belongs to tile k - 2S, this group's own.
+  static constexpr int NBAR = G == 2 ? 2 * STAGES : STAGES;
+  static constexpr size_t smem_bytes() { return (size_t)ES * STAGES * TILE + 8 * NBAR; }
 };
 
 // {acc[i], acc[i+1]} += {a[i], a[i+1]} * s  (a from the constant bank: FFMA2 with a UR pair;
@@ -211,28 +223,40 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tiles = reinterpret_cast<T*>(smem_raw);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(tiles + S * K::TILE);
-  const int tid = threadIdx.x;
-  if (tid == 0)
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+  // group-local thread index: with G = 2 each group runs the whole tile
+  // pipeline on its own tiles, synchronising with a named barrier
+  const int grp = K::G == 1 ? 0 : (int)(threadIdx.x / K::GT);
+  const int tid = (int)threadIdx.x - grp * K::GT;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < K::NBAR; ++s) mbar_init(&bars[s], 1);
   mbar_fence_init();
   __syncthreads();
+  auto group_sync = [&]() {
+    if constexpr (K::G == 1)
+      __syncthreads();
+    else if (grp == 0)  // compile-time barrier ids: a runtime id reserves all 16 per CTA
+      asm volatile("bar.sync 1, %0;" ::"n"(K::GT) : "memory");
+    else
+      asm volatile("bar.sync 2, %0;" ::"n"(K::GT) : "memory");
+  };
 
-  auto issue = [&](long long tile, int stage) {
+  auto issue = [&](long long tile, int stage, int bar = -1) {
     if (tile >= ntiles || tid >= 32) return;
+    if (bar < 0) bar = stage;
     T* dst = tiles + stage * K::TILE;
     const long long first = tile * IT;
     const int valid = (int)(p.batch - first < IT ? p.batch - first : IT);
     if constexpr (K::BULK) {
-      if (tid == 0) mbar_arrive_expect_tx(&bars[stage], (unsigned)(valid * N * NN * sizeof(T)));
+      if (tid == 0) mbar_arrive_expect_tx(&bars[bar], (unsigned)(valid * N * NN * sizeof(T)));
       __syncwarp();
       for (int pl = tid; pl < valid * N; pl += 32) {
         const int e = pl / N, n = pl - e * N;
-        bulk_g2s(dst + e * ITEM + n * PS, p.X + (first + e) * p.sx + (long long)n * NN, NN * sizeof(T), &bars[stage]);
+        bulk_g2s(dst + e * ITEM + n * PS, p.X + (first + e) * p.sx + (long long)n * NN, NN * sizeof(T), &bars[bar]);
       }
     } else if (tid == 0) {
       uintptr_t lo, hi;
       group_span(p.X, p.batch, p.sx, first, valid, lo, hi);
-      span_g2s<T>(dst, lo, hi, &bars[stage]);
+      span_g2s<T>(dst, lo, hi, &bars[bar]);
     }
   };
 
@@ -246,16 +270,29 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
   const int P2 = K::WP ? wid * K::PPW + lid / TPI : K::plane_of_group(tid / TPI);
   const int q2 = K::WP ? lid % TPI : q;
 
+  // CTA-local tile counter k: tile(k) = blockIdx.x + k * gridDim.x; group
+  // k % G runs it in stage k % S (G = 2: refilled by the group that ran k - 3)
+  if constexpr (K::G == 1) {
 #pragma unroll
-  for (int s = 0; s < S - 1; ++s) issue(blockIdx.x + (long long)s * gridDim.x, s);
+    for (int s = 0; s < S - 1; ++s) issue(blockIdx.x + (long long)s * gridDim.x, s);
+  } else if (grp == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) issue(blockIdx.x + (long long)s * gridDim.x, s, s);
+  }
   int stage = 0;
   unsigned phase = 0;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    if constexpr (S == 1)
-      issue(tile, 0);
-    else
-      issue(tile + (long long)(S - 1) * gridDim.x, (stage + S - 1) % S);
-    mbar_wait(&bars[stage], phase);
+  long long kk = grp;
+  for (long long tile = blockIdx.x + kk * gridDim.x; tile < ntiles; tile += (long long)K::G * gridDim.x) {
+    if constexpr (K::G == 1) {
+      if constexpr (S == 1)
+        issue(tile, 0);
+      else
+        issue(tile + (long long)(S - 1) * gridDim.x, (stage + S - 1) % S);
+    } else {
+      stage = (int)(kk % S);
+      phase = (unsigned)((kk / (2 * S)) & 1);
+    }
+    mbar_wait(&bars[K::G == 1 ? stage : (int)(kk % (2 * S))], phase);
     const long long first = tile * IT;
     const int valid = (int)(p.batch - first < IT ? p.batch - first : IT);
     T* buf = tiles + stage * K::TILE;
@@ -275,10 +312,10 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
           m = c / K::PPW;
           cok[k] = c < K::PPW * N && P < NP;
         } else {
-          const int c = tid + k * K::THREADS;
+          const int c = tid + k * K::GT;
           P = c % NP;
           m = c / NP;
-          cok[k] = K::CA * K::THREADS == K::NCOL || c < K::NCOL;
+          cok[k] = K::CA * K::GT == K::NCOL || c < K::NCOL;
         }
         col[k] = buf + (P / N) * ITEM + (P % N) * PS + m * N;
 #pragma unroll
@@ -317,7 +354,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
     if constexpr (K::WP)
       __syncwarp();  // this warp's planes are complete in T1
     else
-      __syncthreads();
+      group_sync();
 
     // ---- mode 2: T2(I_q, j, P2) = sum_m T1(I_q, m, P2) B_r(j, m), in place
     if constexpr (R == 1) {  // one row: FFMA2 pairs columns j, j+1 (uniform B_r pair)
@@ -358,7 +395,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
         }
       }
     }
-    __syncthreads();
+    group_sync();
 
     // ---- mode 3: Y(I_q, j3, k) = init + sum_n T2(I_q, j3, n) Cw(k, n)
     if constexpr (R == 1) {  // one row: FFMA2 pairs k, k+1 (uniform Cw pair)
@@ -412,10 +449,15 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
       }
     }
     fence_proxy_async();  // generic smem writes before the stage's next TMA refill
-    __syncthreads();
-    if (++stage == S) {
-      stage = 0;
-      phase ^= 1;
+    group_sync();
+    if constexpr (K::G == 1) {
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1;
+      }
+    } else {
+      issue(blockIdx.x + (kk + S) * (long long)gridDim.x, stage, (int)((kk + S) % (2 * S)));  // the other group's
+      kk += K::G;
     }
   }
 }

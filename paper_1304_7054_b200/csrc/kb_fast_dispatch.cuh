@@ -203,8 +203,10 @@ static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, 
   if (K::VRY == 2 && (p.ldy % 2 || p.ldy2 % 2 || p.sy % 2 || !aligned<T>(p.Y, 2))) return cudaErrorNotSupported;
   auto kern = p.beta_mode == kBetaZero ? kron3_cw_kernel<T, N, V, true> : kron3_cw_kernel<T, N, V, false>;
   const size_t smem = K::smem_bytes();
-  const int occ = occupancy_for(kern, K::THREADS, smem);
+  int occ = occupancy_for(kern, K::THREADS, smem);
   if (occ <= 0) return cudaErrorNotSupported;
+  static const int force_ctas = env_variant("KB_CW3_CTAS", 0);  // development sweeps: CTAs per SM
+  if (force_ctas > 0 && force_ctas < occ) occ = force_ctas;
   const long long ntiles = (p.batch + K::IT - 1) / K::IT;
   const int grid = (int)(ntiles < (long long)sm_count * occ ? ntiles : (long long)sm_count * occ);
   SqConstsCw3<T, N> kc;
@@ -264,9 +266,13 @@ template <typename T, int N>
 static int k3_family() {
   static const int force = env_variant("KB_K3", -1);
   if (N < 3) return 0;
-  if (force >= 0) return N % 2 && force > 3 && force != 11 && force != 13 ? 0 : force;
+  if (force >= 0) return N % 2 && force > 3 && force != 11 && force != 13 && force != 14 ? 0 : force;
   // fastest family per size, measured on B200 (profiles/r01_k3_families.txt;
   // odd n run the column-wise kernel with span loads)
+  // fp32 n = 14, 16: two 4-warp groups per CTA on a 3-stage ring (V7, 32 warps
+  // per SM instead of 24): +3 % (n = 16, 54.8 -> 56.9 TFLOP/s at 262,144) and
+  // +7-9 % (n = 14) over the 128-thread tiles (profiles/r02_k3_v7.txt)
+  if (sizeof(T) == 4 && (N == 14 || N == 16)) return 14;
   if (sizeof(T) == 4) return N == 8 ? 0 : N == 9 ? 13 : ((N == 11 || N == 14) ? 1 : 3);  // n = 9 warp-plane: +9 %
   if (N == 3 || N == 4) return 0;
   if (N == 12 || N == 14) return 10;  // one row per task: fp64 n = 12 +15 %
@@ -304,12 +310,13 @@ static cudaError_t launch3(const Kron3Params<T>& p, const T* ha, const T* hb, co
       }
     }
 #endif
-    if ((fam >= 1 && fam <= 3) || fam == 10 || fam == 11 || fam == 13) {
+    if ((fam >= 1 && fam <= 3) || fam == 10 || fam == 11 || fam == 13 || fam == 14) {
       const cudaError_t e = fam == 1    ? launch3cw<T, N, 0>(p, ha, hb, hc, sm_count, s)
                             : fam == 2  ? launch3cw<T, N, 1>(p, ha, hb, hc, sm_count, s)
                             : fam == 3  ? launch3cw<T, N, 2>(p, ha, hb, hc, sm_count, s)
                             : fam == 10 ? launch3cw<T, N, 3>(p, ha, hb, hc, sm_count, s)
                             : fam == 11 ? launch3cw<T, N, 4>(p, ha, hb, hc, sm_count, s)
+                            : fam == 14 ? launch3cw<T, N, 7>(p, ha, hb, hc, sm_count, s)
                                         : launch3cw<T, N, 6>(p, ha, hb, hc, sm_count, s);
       if (e != cudaErrorNotSupported) return e;
     }
