@@ -117,7 +117,11 @@ struct Cw3 {
   static constexpr int CA = WP ? (PPW * N + 31) / 32 : (NCOL + GT - 1) / GT;
   static constexpr int STAGES = V == 1 ? 1 : (V == 7 ? 3 : 2);
   // resident CTAs the register budget targets (~24 warps per SM)
-  static constexpr int MINB_AUTO = 768 / ((IT * N * TPI + 31) / 32 * 32) > 0 ? 768 / ((IT * N * TPI + 31) / 32 * 32) : 1;
+  // threads per SM the register budget targets: ~24 warps, except fp32 n = 10
+  // (40 warps at 48 registers, no spills: 35.9 -> 37.3 TFLOP/s; the other
+  // sizes gain nothing or spill, profiles/r02_k3_occupancy.txt)
+  static constexpr int MINT = ES == 4 && N == 10 ? 1280 : 768;
+  static constexpr int MINB_AUTO = MINT / ((IT * N * TPI + 31) / 32 * 32) > 0 ? MINT / ((IT * N * TPI + 31) / 32 * 32) : 1;
   static constexpr int MINB = V == 7 ? 1024 / THREADS
                              : V == 6 ? (768 / THREADS > 0 ? 768 / THREADS : 1)
                              : V == 4 ? MINB_AUTO
