@@ -482,6 +482,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / parity leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer (e2e) legs")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cooldown", type=float, default=3.0,
+                    help="seconds idle before each device-timed workload: each config starts from the same "
+                         "thermal state (a compute-bound config right after the HBM-bound headline otherwise runs "
+                         "under sw_power_cap at ~1750 MHz; clocks are recorded per workload)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -553,8 +557,11 @@ def main():
             fe, be = flops_per_entry(d3, nn), bytes_per_entry(d3, nn, dt)
             l2 = torch.cuda.get_device_properties(devices[0]).L2_cache_size
             sets = 1 if be * bt > 4 * l2 else -(-2 * l2 // (be * bt)) + 1  # rotate > 2x L2 of X/Y between launches
-            xms, xlaunch, _, xpath, xent = time_device(kb, torch, topo, name, max(5, args.steps // 2), args.warmup,
-                                                       sets)
+            time.sleep(args.cooldown)
+            topo.barrier()
+            with ClockSampler(devices) as xclk:
+                xms, xlaunch, _, xpath, xent = time_device(kb, torch, topo, name, max(5, args.steps // 2),
+                                                           args.warmup, sets)
             xtotal = topo.sum(xent)
             part0 = part_batch(topo, sc, bt, 0)
             tf = fe * part0 / (xlaunch * 1e-3) / 1e12
@@ -564,6 +571,7 @@ def main():
             rec = {"workload": name, "scaling": sc, "entries_total": xtotal, "entries_per_gpu": part0,
                    "value": round(fe * xtotal / (xms * 1e-3) / 1e9, 1), "unit": "GFlop/s",
                    "ms_per_step": round(xms, 4), "hbm_gbs": round(gb, 1), "kernel": xpath,
+                   "clocks": xclk.summary(),
                    "l2": ("inputs larger than L2" if sets == 1 else
                           f"{sets} rotating X/Y sets ({sets * be * bt / 1e6:.0f} MB > 2x {l2 / 1e6:.0f} MB L2)"),
                    "roofline": {"bound": "hbm" if roof_tf < fpeak else "fp-pipe", "roof_tflops": round(roof_tf, 2),
