@@ -165,7 +165,16 @@ class Topo:
 
     @property
     def n_gpus(self):
-        return len(set(self.devices)) * self.world
+        if self.world <= 1:
+            return len(set(self.devices))
+        import torch
+        import torch.distributed as dist
+
+        # distinct (host, ordinal) pairs over the job: a rank that reuses another rank's GPU does not count
+        mine = [f"{os.uname().nodename}:{d}" for d in self.devices]
+        every = [None] * self.world
+        dist.all_gather_object(every, mine)
+        return len({x for lst in every for x in lst})
 
     @property
     def total_parts(self):
@@ -422,6 +431,7 @@ def reference_arm(args, rank):
     config, K timed steps after W warm-ups (rank 0 only)."""
     if rank != 0:
         return 0
+    ncores = len(os.sched_getaffinity(0))  # before OpenMP starts and pins this thread (OMP_PROC_BIND)
     from oracle.cpu_ref import OMP_ENV
 
     for k, v in OMP_ENV.items():
@@ -433,6 +443,7 @@ def reference_arm(args, rank):
 
     dims3, n, dtype, batch, _ = WORKLOADS[HEADLINE]
     ref = Reference()
+    ref.set_threads(ncores)  # torchrun exports OMP_NUM_THREADS=1: use every host core
     dt = np.float32
     e = n * n
     a, b, _, x, y = ref.generate_batch(dt, 1, n, dims3, batch)
@@ -502,7 +513,9 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("gloo")  # host barrier + max over ranks only: no NCCL, no data-path collective
-        devices = [local]
+        # one GPU per rank; --devices maps local ranks to ordinals explicitly (e.g. a
+        # two-rank dry run of this path on one GPU: --devices 0,0)
+        devices = [int(args.devices.split(",")[local])] if args.devices else [local]
     elif args.devices:
         devices = [int(d) for d in args.devices.split(",")]
     else:
@@ -601,10 +614,11 @@ def main():
             cpu = {"value": None, "unit": "GFlop/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    n_gpus = topo.n_gpus  # collective under torchrun: every rank takes part
     if rank == 0:
         tr = traffic.get(HEADLINE)
         line = {
-            "metric": METRIC, "value": round(value, 1), "unit": "GFlop/s", "n_gpus": topo.n_gpus,
+            "metric": METRIC, "value": round(value, 1), "unit": "GFlop/s", "n_gpus": n_gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (torch uniform[-1,1); inputs 4.3 GB/GPU >> 126 MB L2, no flush needed)",

@@ -79,6 +79,9 @@ def main(argv=None):
     ap.add_argument("--parity", action="store_true", help="also run the product on the same inputs and compare")
     ap.add_argument("--threads", type=int, default=0)
     args = ap.parse_args(argv)
+    # host cores, read before the OpenMP runtime starts (OMP_PROC_BIND pins the
+    # initial thread to one core once the reference library is loaded)
+    ncores = len(os.sched_getaffinity(0))
 
     for k, v in OMP_ENV.items():
         os.environ.setdefault(k, v)
@@ -94,8 +97,8 @@ def main(argv=None):
     e = n ** (3 if dims3 else 2)
     ref = Reference()
     assert ref.has_openmp, "reference built without OpenMP"
-    if args.threads:
-        ref.set_threads(args.threads)
+    # every host core unless told otherwise (a torchrun parent exports OMP_NUM_THREADS=1)
+    ref.set_threads(args.threads or ncores)
     t0 = time.perf_counter()
     a, b, c, x, y = ref.generate_batch(dt, 1, n, dims3, batch)
     gen_s = time.perf_counter() - t0
