@@ -197,7 +197,7 @@ struct Cw3 {
   // group's load of tile k - S (same stage) has landed; with two barriers the
   // previous phase of k's barrier belongs to tile k - 2S, this group's own.
   static constexpr int NBAR = G == 2 ? 2 * STAGES : STAGES;
-  static constexpr size_t smem_bytes() { return (size_t)ES * STAGES * TILE + 8 * NBAR; }
+  static constexpr size_t smem_bytes() { return (size_t)ES * STAGES * TILE + 8 * NBAR + (G == 2 ? 8 * STAGES : 0); }
 };
 
 // {acc[i], acc[i+1]} += {a[i], a[i+1]} * s  (a from the constant bank: FFMA2 with a UR pair;
@@ -227,6 +227,10 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tiles = reinterpret_cast<T*>(smem_raw);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(tiles + S * K::TILE);
+  // V7 with a tile counter: the tile each stage holds (-1: none left), written
+  // by the issuing lane before its arrive (release) and read after the wait (acquire)
+  long long* stage_tile = reinterpret_cast<long long*>(bars + K::NBAR);
+  const bool dyn = K::G == 2 && p.sched != nullptr;
   // group-local thread index: with G = 2 each group runs the whole tile
   // pipeline on its own tiles, synchronising with a named barrier
   const int grp = K::G == 1 ? 0 : (int)(threadIdx.x / K::GT);
@@ -263,6 +267,23 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
       span_g2s<T>(dst, lo, hi, &bars[bar]);
     }
   };
+  // dynamic scheduling (V7 + p.sched): warp 0 of the calling group takes the
+  // next tile from the call's counter and loads it into `stage` on barrier
+  // `bar`; past the end it publishes -1 with a plain arrive, which releases
+  // the consumer so it can stop
+  auto claim = [&](int stage, int bar) {
+    if (tid >= 32) return;
+    long long t = 0;
+    if (tid == 0) t = (long long)atomicAdd(p.sched, 1ull);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t < ntiles) {
+      if (tid == 0) stage_tile[stage] = t;
+      issue(t, stage, bar);  // lane 0 stores the index before its arrive.expect_tx (release)
+    } else if (tid == 0) {
+      stage_tile[stage] = -1;
+      mbar_arrive(&bars[bar]);
+    }
+  };
 
   // per-thread task coordinates (fixed for the kernel)
   const bool task_ok = tid < K::NTASK;
@@ -281,12 +302,17 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
     for (int s = 0; s < S - 1; ++s) issue(blockIdx.x + (long long)s * gridDim.x, s);
   } else if (grp == 0) {
 #pragma unroll
-    for (int s = 0; s < S; ++s) issue(blockIdx.x + (long long)s * gridDim.x, s, s);
+    for (int s = 0; s < S; ++s) {
+      if (dyn)
+        claim(s, s);
+      else
+        issue(blockIdx.x + (long long)s * gridDim.x, s, s);
+    }
   }
   int stage = 0;
   unsigned phase = 0;
   long long kk = grp;
-  for (long long tile = blockIdx.x + kk * gridDim.x; tile < ntiles; tile += (long long)K::G * gridDim.x) {
+  for (long long tile = blockIdx.x + kk * gridDim.x; dyn || tile < ntiles; tile += (long long)K::G * gridDim.x) {
     if constexpr (K::G == 1) {
       if constexpr (S == 1)
         issue(tile, 0);
@@ -297,6 +323,16 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
       phase = (unsigned)((kk / (2 * S)) & 1);
     }
     mbar_wait(&bars[K::G == 1 ? stage : (int)(kk % (2 * S))], phase);
+    if (dyn) {
+      tile = stage_tile[stage];
+      if (tile < 0) {  // no tiles left: pass the end on to the stage the other group waits on next
+        if (tid == 0) {
+          stage_tile[stage] = -1;
+          mbar_arrive(&bars[(int)((kk + S) % (2 * S))]);
+        }
+        break;
+      }
+    }
     const long long first = tile * IT;
     const int valid = (int)(p.batch - first < IT ? p.batch - first : IT);
     T* buf = tiles + stage * K::TILE;
@@ -460,8 +496,18 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
         phase ^= 1;
       }
     } else {
-      issue(blockIdx.x + (kk + S) * (long long)gridDim.x, stage, (int)((kk + S) % (2 * S)));  // the other group's
+      if (dyn)
+        claim(stage, (int)((kk + S) % (2 * S)));
+      else
+        issue(blockIdx.x + (kk + S) * (long long)gridDim.x, stage, (int)((kk + S) % (2 * S)));  // the other group's
       kk += K::G;
+    }
+  }
+  if (dyn) {  // the last CTA out rewinds the call's counters for the next launch on this lane
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&p.sched[1], 1ull) == gridDim.x - 1) {
+      p.sched[0] = 0;
+      p.sched[1] = 0;
     }
   }
 }

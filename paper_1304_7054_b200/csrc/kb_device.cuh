@@ -89,6 +89,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
   unsigned ok;
   asm volatile(
@@ -269,6 +272,10 @@ struct Kron3Params {
   int opa, opb, opc;
   int beta_mode;
   T alpha, beta;
+  // optional per-call tile counter (device, zeroed before the launch): kernels
+  // that support it take tiles dynamically instead of round-robin, so SMs that
+  // run slower (die / L2-slice distance) do less of the batch
+  unsigned long long* sched = nullptr;
 };
 
 // op-resolved element (i, j) of a stored matrix: op(M)(i, j)

@@ -12,6 +12,7 @@
 #include <memory>
 #include <mutex>
 #include <thread>
+#include <map>
 #include <unordered_map>
 
 namespace kbrt {
@@ -101,7 +102,7 @@ long long stage_bytes() {
 
 namespace {
 
-constexpr int kMaxLanesPerDevice = 32;
+constexpr int kMaxLanesPerDevice = 16;
 
 struct LanePool {
   std::mutex mu;
@@ -183,8 +184,11 @@ static Lane* acquire_lane_impl(int dev, bool capturing) {
       }
     }
     if (!v.empty() && P.created[dev] >= kMaxLanesPerDevice) {
-      wait_for = v.back();  // every idle lane is still in use by async work: wait for the newest
-      v.pop_back();
+      // every idle lane is still in use by async work: wait for the one released
+      // first (its work completes first), so the host stays at most
+      // kMaxLanesPerDevice calls ahead of the device instead of draining it
+      wait_for = v.front();
+      v.erase(v.begin());
     } else {
       auto it = P.sms.find(dev);
       if (it == P.sms.end()) {
@@ -237,6 +241,21 @@ void release_lane(Lane* l, cudaStream_t async_stream) {
   LanePool& P = pool();
   std::lock_guard<std::mutex> lk(P.mu);
   P.idle[l->device].push_back(l);
+}
+
+unsigned long long* stream_counter(int dev, cudaStream_t stream, bool capturing) {
+  static std::mutex mu;
+  static auto* counters = new std::map<std::pair<int, cudaStream_t>, unsigned long long*>;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_pair(dev, stream);
+  auto it = counters->find(key);
+  if (it != counters->end()) return it->second;
+  if (capturing) return nullptr;
+  unsigned long long* c = nullptr;
+  cuda_check(cudaMalloc(&c, 2 * sizeof(unsigned long long)), "tile counter");
+  cuda_check(cudaMemset(c, 0, 2 * sizeof(unsigned long long)), "tile counter");
+  (*counters)[key] = c;
+  return c;
 }
 
 void release_all_lanes() {

@@ -101,6 +101,14 @@ struct LaneLease {
   LaneLease& operator=(const LaneLease&) = delete;
 };
 
+// Tile counter (2 x u64, zero between kernels) of dynamically scheduled kernels
+// launched on `stream` of `dev`: kernels on one stream run one after another,
+// and each one's last CTA rewinds the counter, so one counter per stream is
+// safe and no per-call fencing is needed. Allocated on first use (never
+// freed); nullptr if that first use is inside a CUDA-graph capture (the
+// kernel then schedules statically).
+unsigned long long* stream_counter(int dev, cudaStream_t stream, bool capturing);
+
 // Free every idle lane (all devices). Lanes checked out right now are kept.
 void release_all_lanes();
 // Device bytes held by pooled lanes of `dev` (-1: all devices), for tests.

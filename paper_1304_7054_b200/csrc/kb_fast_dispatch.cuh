@@ -269,10 +269,11 @@ static int k3_family() {
   if (force >= 0) return N % 2 && force > 3 && force != 11 && force != 13 && force != 14 ? 0 : force;
   // fastest family per size, measured on B200 (profiles/r01_k3_families.txt;
   // odd n run the column-wise kernel with span loads)
-  // fp32 n = 14, 16: two 4-warp groups per CTA on a 3-stage ring (V7, 32 warps
-  // per SM instead of 24): +3 % (n = 16, 54.8 -> 56.9 TFLOP/s at 262,144) and
-  // +7-9 % (n = 14) over the 128-thread tiles (profiles/r02_k3_v7.txt)
-  if (sizeof(T) == 4 && (N == 14 || N == 16)) return 14;
+  // fp32 n = 13-16: two 4-warp groups per CTA on a 3-stage ring with dynamic
+  // tile scheduling (V7, 32 warps per SM instead of 24): n = 16 54.8 -> 60.5
+  // TFLOP/s at 262,144, n = 14 +7-9 %, n = 13 / 15 +3-4 % over the 128-thread
+  // tiles (profiles/r02_k3_occupancy.txt)
+  if (sizeof(T) == 4 && N >= 13) return 14;
   if (sizeof(T) == 4) return N == 8 ? 0 : N == 9 ? 13 : ((N == 11 || N == 14) ? 1 : 3);  // n = 9 warp-plane: +9 %
   if (N == 3 || N == 4) return 0;
   if (N == 12 || N == 14) return 10;  // one row per task: fp64 n = 12 +15 %

@@ -826,6 +826,14 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                       cudaGetLastError();
                     }
                   }
+                  if (square_fast) {  // per-stream tile counter for dynamically scheduled kernels
+                    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+                    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+                      cudaGetLastError();
+                      cap = cudaStreamCaptureStatusNone;
+                    }
+                    p.sched = kbrt::stream_counter(r.device, s, cap != cudaStreamCaptureStatusNone);
+                  }
                   cudaError_t e = square_fast
                                       ? kb::launch_kron3_fast<T>(p, ha.data(), hb.data(), hc.data(), r.sm_count, s)
                                       : cudaErrorNotSupported;
