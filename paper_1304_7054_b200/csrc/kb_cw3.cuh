@@ -197,7 +197,7 @@ struct Cw3 {
   // group's load of tile k - S (same stage) has landed; with two barriers the
   // previous phase of k's barrier belongs to tile k - 2S, this group's own.
   static constexpr int NBAR = G == 2 ? 2 * STAGES : STAGES;
-  static constexpr size_t smem_bytes() { return (size_t)ES * STAGES * TILE + 8 * NBAR + (G == 2 ? 8 * STAGES : 0); }
+  static constexpr size_t smem_bytes() { return (size_t)ES * STAGES * TILE + 8 * NBAR + 8 * STAGES; }
 };
 
 // {acc[i], acc[i+1]} += {a[i], a[i+1]} * s  (a from the constant bank: FFMA2 with a UR pair;
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
   // V7 with a tile counter: the tile each stage holds (-1: none left), written
   // by the issuing lane before its arrive (release) and read after the wait (acquire)
   long long* stage_tile = reinterpret_cast<long long*>(bars + K::NBAR);
-  const bool dyn = K::G == 2 && p.sched != nullptr;
+  const bool dyn = p.sched != nullptr;
   // group-local thread index: with G = 2 each group runs the whole tile
   // pipeline on its own tiles, synchronising with a named barrier
   const int grp = K::G == 1 ? 0 : (int)(threadIdx.x / K::GT);
@@ -299,7 +299,12 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
   // k % G runs it in stage k % S (G = 2: refilled by the group that ran k - 3)
   if constexpr (K::G == 1) {
 #pragma unroll
-    for (int s = 0; s < S - 1; ++s) issue(blockIdx.x + (long long)s * gridDim.x, s);
+    for (int s = 0; s < S - 1; ++s) {
+      if (dyn)
+        claim(s, s);
+      else
+        issue(blockIdx.x + (long long)s * gridDim.x, s);
+    }
   } else if (grp == 0) {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -314,7 +319,9 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
   long long kk = grp;
   for (long long tile = blockIdx.x + kk * gridDim.x; dyn || tile < ntiles; tile += (long long)K::G * gridDim.x) {
     if constexpr (K::G == 1) {
-      if constexpr (S == 1)
+      if (dyn)
+        claim(S == 1 ? 0 : (stage + S - 1) % S, S == 1 ? 0 : (stage + S - 1) % S);
+      else if constexpr (S == 1)
         issue(tile, 0);
       else
         issue(tile + (long long)(S - 1) * gridDim.x, (stage + S - 1) % S);
@@ -325,8 +332,8 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
     mbar_wait(&bars[K::G == 1 ? stage : (int)(kk % (2 * S))], phase);
     if (dyn) {
       tile = stage_tile[stage];
-      if (tile < 0) {  // no tiles left: pass the end on to the stage the other group waits on next
-        if (tid == 0) {
+      if (tile < 0) {  // no tiles left
+        if (K::G == 2 && tid == 0) {  // pass the end on to the stage the other group waits on next
           stage_tile[stage] = -1;
           mbar_arrive(&bars[(int)((kk + S) % (2 * S))]);
         }

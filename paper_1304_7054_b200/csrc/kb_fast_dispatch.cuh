@@ -216,7 +216,12 @@ static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, 
       kc.bt[j * kc.LD + i] = hb[i * N + j];  // bt[m*LD + j] = B_r(j, m)
       kc.ct[j * kc.LD + i] = hc[i * N + j];  // ct[n*LD + k] = Cw(k, n)
     }
-  kern<<<grid, K::THREADS, smem, s>>>(p, kc, ntiles);
+  // dynamic tile scheduling (p.sched) pays one L2 atomic per tile: below ~4 KB
+  // of X per tile (fp32 n = 5: 1 KB) the atomic rate on one address becomes the
+  // bottleneck (2.2x slower), so small tiles keep the static round-robin order
+  Kron3Params<T> q = p;
+  if ((long long)K::IT * N * N * N * (long long)sizeof(T) < 4096) q.sched = nullptr;
+  kern<<<grid, K::THREADS, smem, s>>>(q, kc, ntiles);
   return cudaGetLastError();
 }
 

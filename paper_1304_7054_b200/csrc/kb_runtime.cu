@@ -832,7 +832,8 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                       cudaGetLastError();
                       cap = cudaStreamCaptureStatusNone;
                     }
-                    p.sched = kbrt::stream_counter(r.device, s, cap != cudaStreamCaptureStatusNone);
+                    static const bool no_dyn = std::getenv("KB_DYN") && std::getenv("KB_DYN")[0] == '0';  // A/B
+                    p.sched = no_dyn ? nullptr : kbrt::stream_counter(r.device, s, cap != cudaStreamCaptureStatusNone);
                   }
                   cudaError_t e = square_fast
                                       ? kb::launch_kron3_fast<T>(p, ha.data(), hb.data(), hc.data(), r.sm_count, s)
