@@ -510,13 +510,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
       kk += K::G;
     }
   }
-  if (dyn) {  // the last CTA out rewinds the call's counters for the next launch on this lane
-    __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(&p.sched[1], 1ull) == gridDim.x - 1) {
-      p.sched[0] = 0;
-      p.sched[1] = 0;
-    }
-  }
+  if (dyn) sched_rewind(p.sched);  // the last CTA out rewinds the counters for the next launch on the stream
 }
 
 }  // namespace kb

@@ -153,6 +153,16 @@ __device__ __forceinline__ void group_span(const T* X, long long batch, long lon
   hi = a1 < xe ? a1 : xe;
 }
 
+// Dynamic scheduling (Kron3Params::sched): the last CTA to finish rewinds the
+// call's counter pair {next tile, CTAs done} for the next launch on the stream.
+__device__ __forceinline__ void sched_rewind(unsigned long long* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(&ctr[1], 1ull) == gridDim.x - 1) {
+    ctr[0] = 0;
+    ctr[1] = 0;
+  }
+}
+
 // Vector load of W consecutive elements (W*sizeof(T) bytes, naturally aligned).
 template <int W, typename T>
 __device__ __forceinline__ void lds_vec(T* dst, const T* src) {

@@ -192,6 +192,19 @@ std::vector<T> resolve_sq(const std::vector<T>& m, i64 ld, int trans, int n, boo
   return out;
 }
 
+// Per-stream tile counter for the dynamically scheduled kernels (nullptr:
+// static scheduling; KB_DYN=0 forces that for A/B sweeps).
+unsigned long long* sched_counter(int dev, cudaStream_t s) {
+  static const bool off = std::getenv("KB_DYN") && std::getenv("KB_DYN")[0] == '0';
+  if (off) return nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+    cudaGetLastError();
+    cap = cudaStreamCaptureStatusNone;
+  }
+  return kbrt::stream_counter(dev, s, cap != cudaStreamCaptureStatusNone);
+}
+
 void count_launch(const char* path) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   t_last_path = path;
@@ -826,15 +839,7 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                       cudaGetLastError();
                     }
                   }
-                  if (square_fast) {  // per-stream tile counter for dynamically scheduled kernels
-                    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-                    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
-                      cudaGetLastError();
-                      cap = cudaStreamCaptureStatusNone;
-                    }
-                    static const bool no_dyn = std::getenv("KB_DYN") && std::getenv("KB_DYN")[0] == '0';  // A/B
-                    p.sched = no_dyn ? nullptr : kbrt::stream_counter(r.device, s, cap != cudaStreamCaptureStatusNone);
-                  }
+                  if (square_fast) p.sched = sched_counter(r.device, s);
                   cudaError_t e = square_fast
                                       ? kb::launch_kron3_fast<T>(p, ha.data(), hb.data(), hc.data(), r.sm_count, s)
                                       : cudaErrorNotSupported;
