@@ -114,8 +114,16 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
   const long long gw = (long long)blockIdx.x * K::WARPS + warp;
   const long long gstride = (long long)gridDim.x * K::WARPS;
 
+  // ystage with a tight Y whose 16-byte phase matches the stage image: Y
+  // leaves by bulk stores (odd n: one span per group; padded slots: one per
+  // entry) instead of the copy-out loop; a stage is refilled only after the
+  // stores that read it (this lane's bulk groups) have read it
+  const bool ybulk = ystage && p.ldy == N &&
+                     (K::BULK ? (p.sy * (long long)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.Y) & 15) == 0
+                              : p.sy == NN && ((reinterpret_cast<uintptr_t>(p.X) ^ reinterpret_cast<uintptr_t>(p.Y)) & 15) == 0);
   auto issue = [&](long long g, int stage) {
     if (g >= ngroups) return;
+    if (ystage) bulk_wait_read();
     T* dst = wring + stage * K::RING;
     const long long first = g * EPW;
     const int valid = (int)(p.batch - first < EPW ? p.batch - first : EPW);
@@ -243,8 +251,22 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
     }
     }
     if constexpr (ystage) {
-      __syncwarp();
-      copy_out<T, NN, (K::BULK || K::TINY ? K::VXC : 1)>(p.Y + first * p.sy, p.sy, base, SLOT, 0, 1, valid, lane, 32);
+      if (ybulk) {
+        fence_proxy_async();  // staged Y (generic writes) -> the bulk stores (async proxy)
+        __syncwarp();
+        if constexpr (K::BULK) {
+          if (lane < valid) {
+            bulk_s2g(p.Y + (first + lane) * p.sy, base + lane * SLOT, NN * sizeof(T));
+            bulk_commit();
+          }
+        } else {
+          const uintptr_t lo = reinterpret_cast<uintptr_t>(p.Y + first * NN);
+          span_s2g<T>(lo, lo + (uintptr_t)valid * NN * sizeof(T), wring + stage * K::RING, lane);
+        }
+      } else {
+        __syncwarp();
+        copy_out<T, NN, (K::BULK || K::TINY ? K::VXC : 1)>(p.Y + first * p.sy, p.sy, base, SLOT, 0, 1, valid, lane, 32);
+      }
     }
     fence_proxy_async();  // generic smem writes (tmp, staged Y) before the stage's TMA refill
     __syncwarp();
@@ -253,6 +275,7 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
       phase ^= 1;
     }
   }
+  if (ystage) bulk_wait_all();  // the stages stay valid until the last store has read them
 }
 
 }  // namespace kb

@@ -197,7 +197,16 @@ struct Cw3 {
   // group's load of tile k - S (same stage) has landed; with two barriers the
   // previous phase of k's barrier belongs to tile k - 2S, this group's own.
   static constexpr int NBAR = G == 2 ? 2 * STAGES : STAGES;
-  static constexpr size_t smem_bytes() { return (size_t)ES * STAGES * TILE + 8 * NBAR + 8 * STAGES; }
+  // odd n: Y leaves through a per-group shared-memory image of the tile's
+  // output span (its own 16-byte misalignment, <= 16/ES - 1 elements, in
+  // front) and one bulk store, instead of 2 x N scalar 4/8-byte STGs per task
+  // at runtime-strided addresses (p.ystage)
+  static constexpr bool YS = !BULK && R == 2;
+  static constexpr int YTILE = (IT * N * NN + 16 / ES + 16 / ES - 1) / (16 / ES) * (16 / ES);
+  static constexpr size_t YOFF = ((size_t)ES * STAGES * TILE + 8 * NBAR + 8 * STAGES + 15) / 16 * 16;
+  static constexpr size_t smem_bytes(bool ystage = false) {
+    return ystage ? YOFF + (size_t)ES * G * YTILE : (size_t)ES * STAGES * TILE + 8 * NBAR + 8 * STAGES;
+  }
 };
 
 // {acc[i], acc[i+1]} += {a[i], a[i+1]} * s  (a from the constant bank: FFMA2 with a UR pair;
@@ -231,6 +240,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
   // by the issuing lane before its arrive (release) and read after the wait (acquire)
   long long* stage_tile = reinterpret_cast<long long*>(bars + K::NBAR);
   const bool dyn = p.sched != nullptr;
+  const bool ys = K::YS && p.ystage;
   // group-local thread index: with G = 2 each group runs the whole tile
   // pipeline on its own tiles, synchronising with a named barrier
   const int grp = K::G == 1 ? 0 : (int)(threadIdx.x / K::GT);
@@ -239,6 +249,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
     for (int s = 0; s < K::NBAR; ++s) mbar_init(&bars[s], 1);
   mbar_fence_init();
   __syncthreads();
+  T* ysm = reinterpret_cast<T*>(smem_raw + K::YOFF) + grp * K::YTILE;  // this group's Y image (ys)
   auto group_sync = [&]() {
     if constexpr (K::G == 1)
       __syncthreads();
@@ -333,10 +344,9 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
     if (dyn) {
       tile = stage_tile[stage];
       if (tile < 0) {  // no tiles left
-        if (K::G == 2 && tid == 0) {  // pass the end on to the stage the other group waits on next
-          stage_tile[stage] = -1;
-          mbar_arrive(&bars[(int)((kk + S) % (2 * S))]);
-        }
+        // pass the end on: tile kk + S (the other group's next) sits in this
+        // same stage, whose stage_tile already reads -1
+        if (K::G == 2 && tid == 0) mbar_arrive(&bars[(int)((kk + S) % (2 * S))]);
         break;
       }
     }
@@ -442,6 +452,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
         }
       }
     }
+    if (ys && tid == 0) bulk_wait_read();  // the previous tile's Y store has read the image
     group_sync();
 
     // ---- mode 3: Y(I_q, j3, k) = init + sum_n T2(I_q, j3, n) Cw(k, n)
@@ -462,6 +473,8 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
       const bool two = N % 2 == 0 || q * R + 1 < N;
       const T* fb = buf + e3 * ITEM + j3 * N + q * R;
       T* yb = p.Y + (first + e3) * p.sy + (long long)j3 * p.ldy + q * R;
+      // ys: the same element's place in the image (tight Y: ldy = N, ldy2 = NN)
+      T* yi = ysm + (reinterpret_cast<uintptr_t>(p.Y + first * p.sy) & 15) / sizeof(T) + e3 * N * NN + j3 * N + q * R;
       T acc[N][R];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
@@ -487,16 +500,28 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
 #pragma unroll
         for (int k = 0; k < N; ++k) axpy_rows<R>(acc[k], f, kc.ct[n * kc.LD + k]);
       }
+      if (ys) {
 #pragma unroll
-      for (int k = 0; k < N; ++k) {
-        if (K::VRY == 2 || two)
-          stg_n<R, K::VRY>(yb + (long long)k * p.ldy2, acc[k]);
-        else
-          yb[(long long)k * p.ldy2] = acc[k][0];
+        for (int k = 0; k < N; ++k) {
+          yi[k * NN] = acc[k][0];
+          if (two) yi[k * NN + 1] = acc[k][1];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          if (K::VRY == 2 || two)
+            stg_n<R, K::VRY>(yb + (long long)k * p.ldy2, acc[k]);
+          else
+            yb[(long long)k * p.ldy2] = acc[k][0];
+        }
       }
     }
-    fence_proxy_async();  // generic smem writes before the stage's next TMA refill
+    fence_proxy_async();  // generic smem writes before the stage's next TMA refill (and the Y bulk store)
     group_sync();
+    if (ys && tid < 32) {
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(p.Y + first * p.sy);
+      span_s2g<T>(lo, lo + (uintptr_t)valid * N * NN * sizeof(T), ysm, tid);
+    }
     if constexpr (K::G == 1) {
       if (++stage == S) {
         stage = 0;
@@ -510,6 +535,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
       kk += K::G;
     }
   }
+  if (ys && tid == 0) bulk_wait_all();  // the image stays valid until the last store has read it
   if (dyn) sched_rewind(p.sched);  // the last CTA out rewinds the counters for the next launch on the stream
 }
 

@@ -153,6 +153,44 @@ __device__ __forceinline__ void group_span(const T* X, long long batch, long lon
   hi = a1 < xe ? a1 : xe;
 }
 
+// shared -> global bulk copy (TMA engine), tracked by this thread's bulk groups
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// this thread's bulk stores have finished READING shared memory (the source may be rewritten)
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// The store-side twin of span_g2s, run by one warp: global bytes [lo, hi)
+// (element-aligned) from their shared-memory image at src (src <-> lo & ~15,
+// 16-byte aligned; the generic writes that made it are fenced to the async
+// proxy and barrier-ordered before this). Lane 0 stores the 16-byte-aligned
+// interior with one bulk copy (own bulk group: wait with bulk_wait_read before
+// src is rewritten); lanes 1-15 store the unaligned head / tail elements, so
+// nothing outside [lo, hi) -- a neighbouring tile's output -- is written.
+template <typename T>
+__device__ __forceinline__ void span_s2g(uintptr_t lo, uintptr_t hi, const void* src, int lane) {
+  const uintptr_t base = lo & ~uintptr_t(15);
+  const uintptr_t i0 = (lo + 15) & ~uintptr_t(15), i1 = hi & ~uintptr_t(15);
+  const char* s = static_cast<const char*>(src);
+  if (lane == 0) {
+    if (i1 > i0) {
+      bulk_s2g(reinterpret_cast<void*>(i0), s + (i0 - base), static_cast<unsigned>(i1 - i0));
+      bulk_commit();
+    }
+  } else if (lane < 16) {
+    constexpr int E = 16 / sizeof(T);  // elements per 16 bytes
+    const uintptr_t h1 = i0 < hi ? i0 : hi;
+    const int k = (lane - 1) % E;
+    const uintptr_t a = lane <= E ? lo + k * sizeof(T) : (i1 > h1 ? i1 : h1) + k * sizeof(T);
+    if (lane <= 2 * E && (lane <= E ? a < h1 : a < hi))
+      *reinterpret_cast<T*>(a) = *reinterpret_cast<const T*>(s + (a - base));
+  }
+}
+
 // Dynamic scheduling (Kron3Params::sched): the last CTA to finish rewinds the
 // call's counter pair {next tile, CTAs done} for the next launch on the stream.
 __device__ __forceinline__ void sched_rewind(unsigned long long* ctr) {
@@ -286,6 +324,9 @@ struct Kron3Params {
   // that support it take tiles dynamically instead of round-robin, so SMs that
   // run slower (die / L2-slice distance) do less of the batch
   unsigned long long* sched = nullptr;
+  // odd-n column-wise kernels, tight Y: mode 3 writes the tile's Y into a
+  // shared-memory image and one bulk copy per tile stores it (set by the launcher)
+  int ystage = 0;
 };
 
 // op-resolved element (i, j) of a stored matrix: op(M)(i, j)

@@ -406,12 +406,19 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
   const long long gw = (long long)blockIdx.x * K::WARPS + warp;
   const long long gstride = (long long)gridDim.x * K::WARPS;
 
+  // ystage with a tight Y whose 16-byte phase matches the stage image: bulk
+  // stores (odd n: one span per group; padded slots: one per entry) instead of
+  // copy_out; a stage is refilled after this lane's stores have read it
+  const bool ybulk = ystage && use_bar && p.ldy == N &&
+                     (K::BULK ? (p.sy * (long long)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.Y) & 15) == 0
+                              : p.sy == NN && ((reinterpret_cast<uintptr_t>(p.X) ^ reinterpret_cast<uintptr_t>(p.Y)) & 15) == 0);
   // start loading group g (IPW entries) into `stage`
   auto issue = [&](long long g, int stage) {
     if (g >= ngroups) {
       if (!use_bar) cp_async_commit();
       return;
     }
+    if (ystage && use_bar) bulk_wait_read();
     T* dst = wring + stage * K::RING;
     const long long first = g * IPW;
     const int valid = (int)(p.batch - first < IPW ? p.batch - first : IPW);
@@ -481,7 +488,21 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
       __syncwarp();
       const long long first = g * IPW;
       const int valid = (int)(p.batch - first < IPW ? p.batch - first : IPW);
-      copy_out<T, NN, VXC>(p.Y + first * p.sy, p.sy, sbase, C::SLOT, 0, 1, valid, lane, 32);
+      if (ybulk) {
+        fence_proxy_async();  // staged Y (generic writes) -> the bulk stores (async proxy)
+        __syncwarp();
+        if constexpr (K::BULK) {
+          if (lane < valid) {
+            bulk_s2g(p.Y + (first + lane) * p.sy, sbase + lane * C::SLOT, NN * sizeof(T));
+            bulk_commit();
+          }
+        } else {
+          const uintptr_t lo = reinterpret_cast<uintptr_t>(p.Y + first * NN);
+          span_s2g<T>(lo, lo + (uintptr_t)valid * NN * sizeof(T), wring + stage * K::RING, lane);
+        }
+      } else {
+        copy_out<T, NN, VXC>(p.Y + first * p.sy, p.sy, sbase, C::SLOT, 0, 1, valid, lane, 32);
+      }
       if (use_bar) fence_proxy_async();  // generic smem accesses before the TMA refill
     } else if (item < p.batch) {
       T t[N][R];
@@ -506,6 +527,7 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
     }
   }
   if (!use_bar) cp_async_wait<0>();
+  if (ystage && use_bar) bulk_wait_all();  // the stages stay valid until the last store has read them
 }
 
 // ---------------------------------------------------------------- kron3 ---

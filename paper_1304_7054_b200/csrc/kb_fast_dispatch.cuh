@@ -202,7 +202,14 @@ static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, 
     return cudaErrorNotSupported;
   if (K::VRY == 2 && (p.ldy % 2 || p.ldy2 % 2 || p.sy % 2 || !aligned<T>(p.Y, 2))) return cudaErrorNotSupported;
   auto kern = p.beta_mode == kBetaZero ? kron3_cw_kernel<T, N, V, true> : kron3_cw_kernel<T, N, V, false>;
-  const size_t smem = K::smem_bytes();
+  // odd n with a tight Y: stage Y through shared memory and store each tile
+  // with one bulk copy (KB_YS=0 turns it off for A/B sweeps)
+  // (measured: fp32 every odd n +4-23 %; fp64 only n = 7-11 gain, n = 5 / 13 / 15 lose 2-5 %)
+  static const int ys_env = env_variant("KB_YS", -1);
+  const bool ys_on = ys_env >= 0 ? ys_env != 0 : sizeof(T) == 4 || (N >= 7 && N <= 11);
+  Kron3Params<T> q = p;
+  q.ystage = K::YS && ys_on && p.ldy == N && p.ldy2 == (long long)N * N && p.sy == (long long)N * N * N;
+  const size_t smem = K::smem_bytes(q.ystage != 0);
   int occ = occupancy_for(kern, K::THREADS, smem);
   if (occ <= 0) return cudaErrorNotSupported;
   static const int force_ctas = env_variant("KB_CW3_CTAS", 0);  // development sweeps: CTAs per SM
@@ -219,7 +226,6 @@ static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, 
   // dynamic tile scheduling (p.sched) pays one L2 atomic per tile: below ~4 KB
   // of X per tile (fp32 n = 5: 1 KB) the atomic rate on one address becomes the
   // bottleneck (2.2x slower), so small tiles keep the static round-robin order
-  Kron3Params<T> q = p;
   if ((long long)K::IT * N * N * N * (long long)sizeof(T) < 4096) q.sched = nullptr;
   kern<<<grid, K::THREADS, smem, s>>>(q, kc, ntiles);
   return cudaGetLastError();
@@ -274,12 +280,14 @@ static int k3_family() {
   if (force >= 0) return N % 2 && force > 3 && force != 11 && force != 13 && force != 14 ? 0 : force;
   // fastest family per size, measured on B200 (profiles/r01_k3_families.txt;
   // odd n run the column-wise kernel with span loads)
-  // fp32 n = 13-16: two 4-warp groups per CTA on a 3-stage ring with dynamic
+  // fp32 n = 14, 16: two 4-warp groups per CTA on a 3-stage ring with dynamic
   // tile scheduling (V7, 32 warps per SM instead of 24): n = 16 54.8 -> 60.5
-  // TFLOP/s at 262,144, n = 14 +7-9 %, n = 13 / 15 +3-4 % over the 128-thread
-  // tiles (profiles/r02_k3_occupancy.txt)
-  if (sizeof(T) == 4 && N >= 13) return 14;
-  if (sizeof(T) == 4) return N == 8 ? 0 : N == 9 ? 13 : ((N == 11 || N == 14) ? 1 : 3);  // n = 9 warp-plane: +9 %
+  // TFLOP/s at 262,144, n = 14 +7-9 % over the 128-thread tiles
+  // (profiles/r02_k3_occupancy.txt)
+  // odd n with Y staged for bulk stores (p.ystage): fp32 n = 5, 13 one-entry
+  // 256-thread tiles, n = 15 balanced tiles (profiles/r02_k3_occupancy.txt)
+  if (sizeof(T) == 4 && (N == 14 || N == 16)) return 14;
+  if (sizeof(T) == 4) return N == 8 ? 0 : N == 9 ? 13 : ((N == 5 || N == 11 || N == 13) ? 1 : 3);  // n = 9 warp-plane: +9 %
   if (N == 3 || N == 4) return 0;
   if (N == 12 || N == 14) return 10;  // one row per task: fp64 n = 12 +15 %
   if (N == 10) return 11;              // one entry per CTA: +3 %
