@@ -52,12 +52,13 @@ static int env_variant(const char* name, int dflt = 0) {
   return v ? std::atoi(v) : dflt;
 }
 
-// Stage Y through shared memory + coalesced copy-out instead of the direct
-// R-row stores. Measured per size on B200 (profiles/r01_sweep_ystage.txt, r01_sweep2_span.txt):
-// it pays for 2-D wherever the row-block stores are narrow or scattered
-// (fp32: n = 3, 5-11, 15; fp64: n = 3-8, 10, 12) and loses everywhere
-// else, including every 3-D case (the extra CTA barrier costs more than the
-// store coalescing gains). KB_YSTAGE=0 / 1 forces it off / on for sweeps.
+// Stage Y through shared memory (bulk stores when Y is tight, else a
+// coalesced copy-out) instead of the direct R-row stores of the row-owner
+// kernels. Measured per size on B200 (profiles/r01_sweep_ystage.txt,
+// r02_k2_families.txt): it pays for 2-D wherever the row-block stores are
+// narrow or scattered (fp32: n = 3, 5-11, 15; fp64: n = 3-8, 10, 11); the
+// 3-D row-owner kernel never stages (its column-wise siblings do, kb_cw3.cuh).
+// KB_YSTAGE=0 / 1 forces it off / on for sweeps.
 template <typename T, int N, int DIMS>
 static bool want_ystage(bool legal) {
   static const int force = env_variant("KB_YSTAGE", -1);
@@ -65,7 +66,7 @@ static bool want_ystage(bool legal) {
   if (force >= 0) return force != 0;
   if (DIMS == 3) return false;
   if (sizeof(T) == 4) return (N == 3 || (N >= 5 && N <= 11) || N == 15);
-  return (N >= 3 && N <= 8) || N == 10 || N == 12;
+  return (N >= 3 && N <= 8) || N == 10 || N == 11;
 }
 
 template <typename T, int N, int OPX, int V>
@@ -135,10 +136,14 @@ template <typename T, int N>
 static int k2_family() {
   static const int force = env_variant("KB_K2", -1);
   if (force >= 0) return force;
-  // fastest family per size, measured on B200 (profiles/r01_k2_families.txt)
-  if (sizeof(T) == 4) return (N <= 4 || (N >= 9 && N <= 13) || N == 15) ? 1 : 0;
-  if (N == 3 || N == 10 || N == 11 || N == 13) return 2;
-  return (N <= 2 || N == 8 || N == 9) ? 1 : 0;
+  // fastest family per size, measured on B200 (round 2, with staged Y leaving
+  // by bulk stores: profiles/r02_k2_families.txt; round 1: r01_k2_families.txt)
+  if (sizeof(T) == 4) {
+    if (N == 9 || N == 13) return 2;
+    return (N <= 2 || N == 4 || N == 6 || N == 10 || N == 12) ? 1 : 0;
+  }
+  if (N == 3 || N == 5 || N == 10 || N == 12) return 2;
+  return (N <= 2 || N == 8 || N == 9 || N == 13) ? 1 : 0;
 }
 
 template <typename T, int N, int OPX>
