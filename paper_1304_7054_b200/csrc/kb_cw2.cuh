@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
       span_g2s<T>(dst, lo, hi, &wbar[stage]);
     }
   };
+  pdl_enter();  // no global access before the previous kernel on the stream has completed
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) issue(gw + s * gstride, s);
 

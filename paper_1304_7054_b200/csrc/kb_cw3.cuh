@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
   const int P2 = K::WP ? wid * K::PPW + lid / TPI : K::plane_of_group(tid / TPI);
   const int q2 = K::WP ? lid % TPI : q;
 
+  pdl_enter();  // no global access before the previous kernel on the stream has completed
   // CTA-local tile counter k: tile(k) = blockIdx.x + k * gridDim.x; group
   // k % G runs it in stage k % S (G = 2: refilled by the group that ran k - 3)
   if constexpr (K::G == 1) {

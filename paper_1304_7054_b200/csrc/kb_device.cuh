@@ -191,6 +191,19 @@ __device__ __forceinline__ void span_s2g(uintptr_t lo, uintptr_t hi, const void*
   }
 }
 
+// Programmatic dependent launch: kernels launched with the programmatic
+// stream-serialization attribute (kb_fast_dispatch.cuh launch_pdl) may be
+// scheduled while the previous kernel on the stream drains its last CTAs, so
+// their launch latency and prologue (barrier init, constant staging) overlap
+// that tail. griddepcontrol.wait blocks until the previous grid has completed
+// and its memory is visible -- every global access of the kernel comes after
+// it, so stream order is kept exactly; launch_dependents lets the NEXT kernel
+// start its own prologue. Both are no-ops without the attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Dynamic scheduling (Kron3Params::sched): the last CTA to finish rewinds the
 // call's counter pair {next tile, CTAs done} for the next launch on the stream.
 __device__ __forceinline__ void sched_rewind(unsigned long long* ctr) {

@@ -445,6 +445,7 @@ __global__ void __launch_bounds__(Kron2Fast<T, N, V>::WARPS * 32)
     }
   };
 
+  pdl_enter();  // no global access before the previous kernel on the stream has completed
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) issue(gw + s * gstride, s);
 

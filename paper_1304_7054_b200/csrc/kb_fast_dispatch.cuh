@@ -6,6 +6,7 @@
 #include <mutex>
 #include <cstdlib>
 #include <map>
+#include <tuple>
 #include <utility>
 
 #include "kb_cw2.cuh"
@@ -22,22 +23,32 @@ namespace kb {
 // of one template share a function-pointer type).
 template <typename Kern>
 static int occupancy_for(Kern kern, int threads, size_t smem) {
+  // a kernel can be launched with more than one dynamic smem size (kb_cw3's
+  // Y image is only reserved for tight Y): occupancy is cached per size, and
+  // the opt-in limit is only ever RAISED, to the largest size seen, so a
+  // launch with a size seen earlier stays valid
   static std::mutex mu;
-  static std::map<std::pair<const void*, int>, int> cache;
+  static std::map<std::tuple<const void*, int, size_t>, int> cache;
+  static std::map<std::pair<const void*, int>, size_t> limit;
   std::lock_guard<std::mutex> lock(mu);
   int dev = 0;
   cudaGetDevice(&dev);
-  const auto dkey = std::make_pair(reinterpret_cast<const void*>(kern), dev);
-  auto it = cache.find(dkey);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), dev, smem);
+  auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int occ = 0;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaSuccess;
+  size_t& lim = limit[std::make_pair(reinterpret_cast<const void*>(kern), dev)];
+  if (smem > lim) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) lim = smem;
+  }
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   if (e != cudaSuccess) {
     cudaGetLastError();
     occ = 0;
   }
-  cache[dkey] = occ;
+  cache[key] = occ;
   return occ;
 }
 
@@ -50,6 +61,26 @@ static bool aligned(const void* p, int elems) {
 static int env_variant(const char* name, int dflt = 0) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
+}
+
+// Launch with programmatic stream serialization (PDL, see pdl_enter in
+// kb_device.cuh) for the kernels that call pdl_enter() before touching global
+// memory. KB_PDL=0 launches them plainly (A/B sweeps).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int threads, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  static const int pdl = env_variant("KB_PDL", 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // Stage Y through shared memory (bulk stores when Y is tight, else a
@@ -92,8 +123,7 @@ static cudaError_t launch2v(const Kron2Params<T>& p, const T* ha, const T* hw, i
     kc.a[i] = ha[i];
     kc.w[i] = hw[i];
   }
-  kern<<<grid, threads, smem, s>>>(p, kc, ngroups);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, threads, smem, s, p, kc, ngroups);
 }
 
 // Column-wise 2-D kernel (kb_cw2.cuh), op_x = N. ys: Y staged through smem.
@@ -125,8 +155,7 @@ static cudaError_t launch2cw(const Kron2Params<T>& p, const T* ha, const T* hw, 
   for (int l = 0; l < N; ++l)
     for (int i = 0; i < N; ++i) kc.a[l * kc.LD + i] = ha[l * N + i];
   for (int i = 0; i < N * N; ++i) kc.w[i] = hw[i];
-  kern<<<grid, threads, smem, s>>>(p, kc, ngroups);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, threads, smem, s, p, kc, ngroups);
 }
 
 // 2-D kernel family per size: 0 = row-owner kron2_sq_kernel, 1 = column-wise
@@ -228,12 +257,12 @@ static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, 
       kc.bt[j * kc.LD + i] = hb[i * N + j];  // bt[m*LD + j] = B_r(j, m)
       kc.ct[j * kc.LD + i] = hc[i * N + j];  // ct[n*LD + k] = Cw(k, n)
     }
-  // dynamic tile scheduling (p.sched) pays one L2 atomic per tile: below ~4 KB
-  // of X per tile (fp32 n = 5: 1 KB) the atomic rate on one address becomes the
-  // bottleneck (2.2x slower), so small tiles keep the static round-robin order
-  if ((long long)K::IT * N * N * N * (long long)sizeof(T) < 4096) q.sched = nullptr;
-  kern<<<grid, K::THREADS, smem, s>>>(q, kc, ntiles);
-  return cudaGetLastError();
+  // dynamic tile scheduling (p.sched) pays one L2 atomic per tile on one
+  // address: at <= 4 KB of X per tile (> 1.5 G tiles/s at HBM speed; fp32 n = 5
+  // 1 KB tiles: 2.2x slower, fp64 n = 8 4 KB one-warp tiles: 2x slower) that
+  // atomic rate is the bottleneck, so small tiles keep the static round-robin order
+  if ((long long)K::IT * N * N * N * (long long)sizeof(T) <= 4096) q.sched = nullptr;
+  return launch_pdl(kern, grid, K::THREADS, smem, s, q, kc, ntiles);
 }
 
 #ifdef KB_SWEEP_VARIANTS  // n = 16 warp-plane experiments, kept out of the product tree

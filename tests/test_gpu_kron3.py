@@ -271,3 +271,43 @@ def test_baseline_configs_sampled_oracle(dtype, batch):
         o.kron3("N", "N", "N", n, n, n, n, n, n, 1, dtype(1), a, n, b, n, c, n, x[s], n, n * n, e, dtype(0), yo, n,
                 n * n, e)
         assert mismatches(got[s], yo) == 0
+
+
+_SMEM_ORDER = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import paper_1304_7054_b200 as kb
+from kb_testutil import mismatches, oracle, to_dev, to_host
+o = oracle()
+n, batch = 13, 41
+e = n ** 3
+for dt in (np.float32, np.float64):
+    for pad in (5, 0):  # padded Y entry stride first (no Y image), then tight (Y image: more smem)
+        a, b, c, x, y = o.generate_batch(dt, 1, n, True, batch)
+        sy = e + pad
+        y0 = np.zeros(sy * batch, dt)
+        want = y0.copy()
+        X, Y = to_dev(x), to_dev(y0)
+        pr = kb.KronProblem3D(m_a=n, n_a=n, m_b=n, n_b=n, m_c=n, n_c=n)
+        kb.kron3(pr, kb.MatrixView(to_dev(a), n, n, n), kb.MatrixView(to_dev(b), n, n, n), kb.MatrixView(to_dev(c), n, n, n),
+                 kb.BatchView(kb.Array3View(X, n, n, n, n, n * n), batch, e),
+                 kb.BatchView(kb.Array3View(Y, n, n, n, n, n * n), batch, sy), kb.Workspace(None, e * batch))
+        o.kron3("N", "N", "N", n, n, n, n, n, n, batch, dt(1), a, n, b, n, c, n, x, n, n * n, e, dt(0), want, n, n * n, sy)
+        assert mismatches(to_host(Y), want) == 0, (dt, pad)
+print("OK")
+"""
+
+
+def test_same_kernel_two_smem_sizes_fresh_process():
+    """One kernel, two dynamic shared-memory sizes in one process: the odd-n
+    column-wise kernel reserves its Y image only for a tight Y, so a padded-Y
+    call followed by a tight one needs the opt-in smem limit raised (a cache
+    keyed by kernel alone launched the second with 'invalid argument')."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _SMEM_ORDER, root], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
