@@ -314,17 +314,19 @@ static int k3_family() {
   if (force >= 0) return N % 2 && force > 3 && force != 11 && force != 13 && force != 14 ? 0 : force;
   // fastest family per size, measured on B200 (profiles/r01_k3_families.txt;
   // odd n run the column-wise kernel with span loads)
-  // fp32 n = 14, 16: two 4-warp groups per CTA on a 3-stage ring with dynamic
-  // tile scheduling (V7, 32 warps per SM instead of 24): n = 16 54.8 -> 60.5
-  // TFLOP/s at 262,144, n = 14 +7-9 % over the 128-thread tiles
-  // (profiles/r02_k3_occupancy.txt)
-  // odd n with Y staged for bulk stores (p.ystage): fp32 n = 5, 13 one-entry
-  // 256-thread tiles, n = 15 balanced tiles (profiles/r02_k3_occupancy.txt)
-  if (sizeof(T) == 4 && (N == 14 || N == 16)) return 14;
-  if (sizeof(T) == 4) return N == 8 ? 0 : N == 9 ? 13 : ((N == 5 || N == 11 || N == 13) ? 1 : 3);  // n = 9 warp-plane: +9 %
+  // fp32 n = 16: two 4-warp groups per CTA on a 3-stage ring with dynamic
+  // tile scheduling (V7, 32 warps per SM instead of 24): 54.8 -> 60.5 TFLOP/s
+  // at 262,144 (profiles/r02_k3_occupancy.txt)
+  // odd n with Y staged for bulk stores (p.ystage): fp32 n = 5, 13 256-thread
+  // tiles, n = 15 balanced tiles; with dynamic scheduling fp32 n = 14 is
+  // fastest on the 256-thread tiles (42.0 vs 37.0 TFLOP/s for V7), fp64 n = 16
+  // with one row per task (28.1 vs 26.0), fp64 n = 15 on balanced tiles (+5 %)
+  if (sizeof(T) == 4 && N == 16) return 14;
+  if (sizeof(T) == 4) return N == 8 ? 0 : N == 9 ? 13 : ((N == 5 || N == 11 || N == 13 || N == 14) ? 1 : 3);  // n = 9 warp-plane: +9 %
   if (N == 3 || N == 4) return 0;
-  if (N == 12 || N == 14) return 10;  // one row per task: fp64 n = 12 +15 %
-  if (N == 10) return 11;              // one entry per CTA: +3 %
+  if (N == 12 || N == 14 || N == 16) return 10;  // one row per task: fp64 n = 12 +15 %
+  if (N == 10) return 11;                         // one entry per CTA: +3 %
+  if (N == 15) return 3;
   return N <= 7 ? 1 : 2;
 }
 
