@@ -161,6 +161,50 @@ __global__ void __launch_bounds__(256) repack_kernel(const T* __restrict__ src, 
   }
 }
 
+// Square entries (n <= 16, the repack path of the fast kernels): the same copy
+// with the entry shape a compile-time constant, so the per-element index split
+// is multiply-shift instead of runtime 64-/32-bit divisions (which bound the
+// generic kernel at ~0.6 TB/s).
+template <typename T, int N, int D3>
+__global__ void __launch_bounds__(256) repack_sq_kernel(const T* __restrict__ src, long long s_ld, long long s_ld2,
+                                                        long long s_stride, T* __restrict__ dst, long long d_ld,
+                                                        long long d_ld2, long long d_stride, long long total) {
+  constexpr unsigned PER = N * N * D3;
+  pdl_enter();  // launched with programmatic serialization: the previous kernel's tail overlaps this launch
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long ut = (unsigned long long)t;
+    const long long p = (long long)(ut / PER);
+    const unsigned r = (unsigned)(ut - (unsigned long long)p * PER);
+    const unsigned i = r % N, jk = r / N, j = jk % N, k = jk / N;
+    dst[p * d_stride + i + j * d_ld + k * d_ld2] = src[p * s_stride + i + j * s_ld + k * s_ld2];
+  }
+}
+
+template <typename T, int N>
+static bool launch_repack_sq(const T* src, long long s_ld, long long s_ld2, long long s_stride, T* dst, long long d_ld,
+                             long long d_ld2, long long d_stride, int n, int d3, long long total, int grid,
+                             cudaStream_t s) {
+  if constexpr (N > 1) {
+    if (n != N) return launch_repack_sq<T, N - 1>(src, s_ld, s_ld2, s_stride, dst, d_ld, d_ld2, d_stride, n, d3, total,
+                                                  grid, s);
+  } else if (n != 1) {
+    return false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256u);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto kern = d3 == 1 ? repack_sq_kernel<T, N, 1> : repack_sq_kernel<T, N, N>;
+  cudaLaunchKernelEx(&cfg, kern, src, s_ld, s_ld2, s_stride, dst, d_ld, d_ld2, d_stride, total);
+  return true;
+}
+
 template <typename T>
 cudaError_t launch_repack(const T* src, long long s_ld, long long s_ld2, long long s_stride, T* dst, long long d_ld,
                           long long d_ld2, long long d_stride, int d1, int d2, int d3, long long batch, int sm_count,
@@ -168,8 +212,11 @@ cudaError_t launch_repack(const T* src, long long s_ld, long long s_ld2, long lo
   const long long total = batch * d1 * d2 * d3;
   if (total <= 0) return cudaSuccess;
   const long long want = (total + 255) / 256, cap = (long long)sm_count * 16;
-  repack_kernel<T><<<(int)(want < cap ? want : cap), 256, 0, s>>>(src, s_ld, s_ld2, s_stride, dst, d_ld, d_ld2,
-                                                                    d_stride, d1, d2, d3, total);
+  const int grid = (int)(want < cap ? want : cap);
+  if (d1 == d2 && d1 >= 1 && d1 <= 16 && (d3 == 1 || d3 == d1) &&
+      launch_repack_sq<T, 16>(src, s_ld, s_ld2, s_stride, dst, d_ld, d_ld2, d_stride, d1, d3, total, grid, s))
+    return cudaGetLastError();
+  repack_kernel<T><<<grid, 256, 0, s>>>(src, s_ld, s_ld2, s_stride, dst, d_ld, d_ld2, d_stride, d1, d2, d3, total);
   return cudaGetLastError();
 }
 

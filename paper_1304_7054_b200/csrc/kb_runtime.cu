@@ -226,17 +226,20 @@ struct K2 {
 // Square n <= 16 on a padded / strided layout the fast kernels cannot stream
 // (ld != n, ragged entry strides): repack each chunk into tight lane buffers,
 // run the fast kernel there, repack Y back (entry elements only: padding is
-// never written). Chunks of <= 32 MiB per side stay resident in the 126 MB L2
-// between the three kernels, so HBM mostly sees X once and Y once; same
-// per-element arithmetic as the generic kernel (bit-identical).
-constexpr i64 kRepackBytes = i64(32) << 20;
+// never written). Chunks of <= 64 MiB per side (measured: 8 / 16 / 32 / 64 MiB
+// -> 2.8 / 2.3 / 2.1 / 2.1 ms per GiB at 2-D fp32 n = 10; fewer, longer
+// launches win over strict L2 residency); same per-element arithmetic as the
+// generic kernel (bit-identical).
+constexpr i64 kRepackBytes = i64(64) << 20;
 
 template <typename T, typename Fast>
 void run_repacked(int dims, int N, const T* X, i64 ldx, i64 ldx2, i64 sx, T* Y, i64 ldy, i64 ldy2, i64 sy,
                   bool y_in, i64 n, Lane& r, cudaStream_t s, int slot, Fast&& fast) {
   const i64 e = dims == 3 ? (i64)N * N * N : (i64)N * N;
   const int d3 = dims == 3 ? N : 1;
-  const i64 chunk = std::max<i64>(1, std::min<i64>(n, kRepackBytes / (e * (i64)sizeof(T))));
+  static const i64 repack_bytes = std::getenv("KB_REPACK_MB") ? (i64)std::atoi(std::getenv("KB_REPACK_MB")) << 20
+                                                                 : kRepackBytes;  // A/B sweeps
+  const i64 chunk = std::max<i64>(1, std::min<i64>(n, repack_bytes / (e * (i64)sizeof(T))));
   T* xt = static_cast<T*>(r.use(r.pk[0][slot]).get(sizeof(T) * (size_t)(chunk * e)));
   T* yt = static_cast<T*>(r.use(r.pk[1][slot]).get(sizeof(T) * (size_t)(chunk * e)));
   for (i64 q0 = 0; q0 < n; q0 += chunk) {
