@@ -161,23 +161,44 @@ __global__ void __launch_bounds__(256) repack_kernel(const T* __restrict__ src, 
   }
 }
 
-// Square entries (n <= 16, the repack path of the fast kernels): the same copy
-// with the entry shape a compile-time constant, so the per-element index split
-// is multiply-shift instead of runtime 64-/32-bit divisions (which bound the
-// generic kernel at ~0.6 TB/s).
+// Square entries (n <= 16, the repack path of the fast kernels): the entry
+// shape is compile-time, and a CTA walks groups of EPB whole entries (~2K
+// elements) with a FIXED per-thread set of U element slots, so the index split
+// and the in-entry offsets of both layouts are computed once per thread; per
+// element only the group base moves (thread per element in tight order: the
+// tight side is fully coalesced, the strided side reads / writes runs of n).
 template <typename T, int N, int D3>
 __global__ void __launch_bounds__(256) repack_sq_kernel(const T* __restrict__ src, long long s_ld, long long s_ld2,
                                                         long long s_stride, T* __restrict__ dst, long long d_ld,
-                                                        long long d_ld2, long long d_stride, long long total) {
-  constexpr unsigned PER = N * N * D3;
+                                                        long long d_ld2, long long d_stride, long long batch) {
+  constexpr int PER = N * N * D3;
+  constexpr int EPB = PER >= 2048 ? 1 : 2048 / PER;  // entries per group
+  constexpr int TOT = EPB * PER;
+  constexpr int U = (TOT + 255) / 256;
+  long long soff[U], doff[U];
+  int eix[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int t = (int)threadIdx.x + 256 * u;
+    const int e = t / PER, r = t - e * PER;
+    const int i = r % N, jk = r / N, j = jk % N, k = jk / N;
+    eix[u] = t < TOT ? e : EPB;  // EPB: slot unused
+    soff[u] = e * s_stride + i + j * s_ld + k * s_ld2;
+    doff[u] = e * d_stride + i + j * d_ld + k * d_ld2;
+  }
   pdl_enter();  // launched with programmatic serialization: the previous kernel's tail overlaps this launch
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const unsigned long long ut = (unsigned long long)t;
-    const long long p = (long long)(ut / PER);
-    const unsigned r = (unsigned)(ut - (unsigned long long)p * PER);
-    const unsigned i = r % N, jk = r / N, j = jk % N, k = jk / N;
-    dst[p * d_stride + i + j * d_ld + k * d_ld2] = src[p * s_stride + i + j * s_ld + k * s_ld2];
+  for (long long g = blockIdx.x; g * EPB < batch; g += gridDim.x) {
+    const long long p0 = g * EPB;
+    const int left = batch - p0 < EPB ? (int)(batch - p0) : EPB;
+    const T* sg = src + p0 * s_stride;
+    T* dg = dst + p0 * d_stride;
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (eix[u] < left) v[u] = sg[soff[u]];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (eix[u] < left) dg[doff[u]] = v[u];
   }
 }
 
@@ -201,7 +222,10 @@ static bool launch_repack_sq(const T* src, long long s_ld, long long s_ld2, long
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   auto kern = d3 == 1 ? repack_sq_kernel<T, N, 1> : repack_sq_kernel<T, N, N>;
-  cudaLaunchKernelEx(&cfg, kern, src, s_ld, s_ld2, s_stride, dst, d_ld, d_ld2, d_stride, total);
+  const long long per = (long long)N * N * (d3 == 1 ? 1 : N), epb = per >= 2048 ? 1 : 2048 / per;
+  const long long batch = total / per, groups = (batch + epb - 1) / epb;
+  cfg.gridDim = dim3((unsigned)(groups < grid ? groups : grid));
+  cudaLaunchKernelEx(&cfg, kern, src, s_ld, s_ld2, s_stride, dst, d_ld, d_ld2, d_stride, batch);
   return true;
 }
 
