@@ -137,6 +137,7 @@ void destroy_lane(Lane* l) {
   cudaStreamSynchronize(l->stream);
   for (auto& s : l->slot_stream) cudaStreamSynchronize(s);
   l->consts.release();
+  l->hconsts.release();
   for (int i = 0; i < kSlots; ++i) {
     l->scratch[i].release();
     l->xs[i].release();

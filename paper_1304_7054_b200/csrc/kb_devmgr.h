@@ -70,6 +70,7 @@ struct Lane {
   DevBuf xs[kSlots], ys[kSlots];                // device staging (host-resident X / Y)
   HostBuf hx[kSlots], hy[kSlots];               // pinned bounce buffers (pageable X / Y)
   DevBuf pk[2][kSlots];                         // tight X / Y for padded square calls (repack path)
+  HostBuf hconsts;                              // pinned landing of device-resident constant matrices
   bool used = false;  // this checkout handed a device buffer (constants / scratch) to a kernel
   DevBuf& use(DevBuf& b) {
     used = true;

@@ -11,6 +11,7 @@
 // and keeps L0 validation semantics (views.hpp:172-240) and the L2 control
 // flow (kron2.hpp:41-79, kron3.hpp:77-128) bit-for-bit in behaviour.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -158,18 +159,41 @@ const T* const_on_device(const T* m, i64 elems, int dev, T* slot, cudaStream_t s
   return slot;
 }
 
-// Host copy of a small constant matrix (device -> host copy when needed; this
-// synchronises the stream, which only the square fast path requires).
-template <typename T>
-std::vector<T> fetch_host(const T* m, i64 elems, cudaStream_t s) {
-  std::vector<T> h((size_t)std::max<i64>(elems, 1));
-  if (elems <= 0) return h;
-  const PtrInfo pi = classify(m);
-  if (pi.device) {
-    cuda_check(cudaMemcpyAsync(h.data(), m, sizeof(T) * (size_t)elems, cudaMemcpyDeviceToHost, s), "constant fetch");
+// Host copies of the small constant matrices the square fast path folds into
+// kernel parameters. Host-resident ones are plain copies; device-resident ones
+// land by async copies in the lane's pinned buffer and ONE stream
+// synchronisation covers all of them (a pageable copy + synchronisation per
+// matrix cost ~10 us each). Keeping A/B/C on the host, as the reference's
+// callers do, avoids the synchronisation altogether.
+template <typename T, size_t K>
+std::array<std::vector<T>, K> fetch_host(const std::array<const T*, K>& ms, const std::array<i64, K>& elems, Lane& r,
+                                         cudaStream_t s) {
+  std::array<std::vector<T>, K> h;
+  size_t dev_bytes = 0;
+  std::array<bool, K> on_dev{};
+  for (size_t i = 0; i < K; ++i) {
+    h[i].assign((size_t)std::max<i64>(elems[i], 1), T(0));
+    if (elems[i] <= 0) continue;
+    on_dev[i] = classify(ms[i]).device;
+    if (on_dev[i]) dev_bytes += sizeof(T) * (size_t)elems[i];
+    else std::memcpy(h[i].data(), ms[i], sizeof(T) * (size_t)elems[i]);
+  }
+  if (dev_bytes) {
+    char* pin = static_cast<char*>(r.hconsts.get(dev_bytes));
+    size_t off = 0;
+    for (size_t i = 0; i < K; ++i)
+      if (on_dev[i]) {
+        cuda_check(cudaMemcpyAsync(pin + off, ms[i], sizeof(T) * (size_t)elems[i], cudaMemcpyDeviceToHost, s),
+                   "constant fetch");
+        off += sizeof(T) * (size_t)elems[i];
+      }
     cuda_check(cudaStreamSynchronize(s), "constant fetch");
-  } else {
-    std::memcpy(h.data(), m, sizeof(T) * (size_t)elems);
+    off = 0;
+    for (size_t i = 0; i < K; ++i)
+      if (on_dev[i]) {
+        std::memcpy(h[i].data(), pin + off, sizeof(T) * (size_t)elems[i]);
+        off += sizeof(T) * (size_t)elems[i];
+      }
   }
   return h;
 }
@@ -529,8 +553,9 @@ int kron2_entry(char ta, char tb, char tx, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
             if (!square_fast) upload(r, s);
             if (square_fast) {
               const i64 fa = fp_matrix(ac, lda), fb = fp_matrix(bc, ldb);
-              ha = resolve_sq(fetch_host(A, fa, s), lda, is_t(ta), (int)m_a, false, T(1), false);
-              hw = resolve_sq(fetch_host(B, fb, s), ldb, is_t(tb), (int)m_a, true, alpha, true);
+              const auto h = fetch_host<T, 2>({A, B}, {fa, fb}, r, s);
+              ha = resolve_sq(h[0], lda, is_t(ta), (int)m_a, false, T(1), false);
+              hw = resolve_sq(h[1], ldb, is_t(tb), (int)m_a, true, alpha, true);
             }
           },
           [&](const void* xd, void* yd, i64 n, Lane& r, cudaStream_t s, int slot) {
@@ -605,7 +630,7 @@ int kron1_entry(char ta, i64 m_a, i64 n_a, i64 batch, T alpha, const T* A, i64 l
             if (scale_only) return;  // A, X never read (kron1.hpp:45-55)
             const i64 fa = fp_matrix(ac, lda);
             if (square_fast) {
-              ha = resolve_sq(fetch_host(A, fa, s), lda, is_t(ta), (int)m_a, false, T(1), false);
+              ha = resolve_sq(fetch_host<T, 1>({A}, {fa}, r, s)[0], lda, is_t(ta), (int)m_a, false, T(1), false);
               return;
             }
             T* cs = static_cast<T*>(r.use(r.consts).get(sizeof(T) * (size_t)(fa + 32)));
@@ -683,7 +708,7 @@ int gemm_a_entry(char ta, char tb, i64 m, i64 n, i64 k, i64 batch, T alpha, cons
             if (scale_only) return;  // A, B never read (gemm_a.hpp:46-58)
             const i64 fb = fp_matrix(bc, ldb);
             if (square_fast) {  // w(kk, c) = op(B)(kk, c), times alpha for gemm_axpy (detail.hpp:53)
-              hw = resolve_sq(fetch_host(B, fb, s), ldb, is_t(tb), (int)m, false, alpha, !is_t(ta));
+              hw = resolve_sq(fetch_host<T, 1>({B}, {fb}, r, s)[0], ldb, is_t(tb), (int)m, false, alpha, !is_t(ta));
               return;
             }
             T* cs = static_cast<T*>(r.use(r.consts).get(sizeof(T) * (size_t)(fb + 32)));
@@ -808,9 +833,10 @@ int kron3_entry(char ta, char tb, char tc, i64 m_a, i64 n_a, i64 m_b, i64 n_b, i
                   // parameters, so square calls skip the uploads (lazy below)
                   if (!square_fast) upload();
                   if (square_fast) {
-                    ha = resolve_sq(fetch_host(A, fa, s), lda, is_t(ta), (int)m_a, false, T(1), false);
-                    hb = resolve_sq(fetch_host(B, fb, s), ldb, is_t(tb), (int)m_a, true, T(1), false);
-                    hc = resolve_sq(fetch_host(Cm, fc, s), ldc, is_t(tc), (int)m_a, true, alpha, true);
+                    const auto h = fetch_host<T, 3>({A, B, Cm}, {fa, fb, fc}, r, s);
+                    ha = resolve_sq(h[0], lda, is_t(ta), (int)m_a, false, T(1), false);
+                    hb = resolve_sq(h[1], ldb, is_t(tb), (int)m_a, true, T(1), false);
+                    hc = resolve_sq(h[2], ldc, is_t(tc), (int)m_a, true, alpha, true);
                   }
                 },
                 [&](const void* xd, void* yd, i64 n, Lane& r, cudaStream_t s, int slot) {
