@@ -18,7 +18,7 @@ OBJS      := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS)) $(OBJDIR)/kb_hostcop
 HDRS      := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/kronbatch_b200.h
 LIB       := $(PKG)/libkronbatch_b200.so
 
-.PHONY: all lib oracle accept cpptest kronbench sanitize clean
+.PHONY: all lib oracle accept cpptest kronbench sanitize microbench clean
 all: lib oracle
 
 lib: $(LIB)
@@ -53,6 +53,13 @@ sanitize: build/sanitize/kb_sanitize
 build/sanitize/kb_sanitize: tools/sanitize/kb_sanitize.cpp $(LIB) include/kronbatch_b200.h
 	@mkdir -p build/sanitize
 	$(CXX_HOST) -O2 -std=gnu++17 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -lkronbatch_b200 \
+	  -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
+
+# host cost of one call through the C ABI (development aid)
+microbench: build/microbench/call_overhead
+build/microbench/call_overhead: tools/microbench/call_overhead.cpp $(LIB) include/kronbatch_b200.h
+	@mkdir -p build/microbench
+	$(CXX_HOST) -O2 -std=c++17 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -lkronbatch_b200 \
 	  -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
 
 # native bench CLI (the reference's `bench` flags + CSV schema, on the B200 library)
