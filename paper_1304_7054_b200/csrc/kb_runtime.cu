@@ -179,6 +179,12 @@ std::array<std::vector<T>, K> fetch_host(const std::array<const T*, K>& ms, cons
     else std::memcpy(h[i].data(), ms[i], sizeof(T) * (size_t)elems[i]);
   }
   if (dev_bytes) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (s && cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+      throw Fail{KB_EINVAL,
+                 "device-resident constant matrices cannot be folded into the kernel parameters during CUDA-graph "
+                 "capture (that needs a synchronisation); pass A/B/C in host memory"};
+    cudaGetLastError();
     char* pin = static_cast<char*>(r.hconsts.get(dev_bytes));
     size_t off = 0;
     for (size_t i = 0; i < K; ++i)

@@ -287,3 +287,69 @@ def test_pageable_padded_y_padding_untouched_kron3():
     want = np.full(sy * batch, -3.25)
     o.kron3("N", "N", "N", n, n, n, n, n, n, batch, 1.0, a, n, b, n, c, n, x, n, n * n, n ** 3, 0.0, want, ld, ld2, sy)
     assert mismatches(y, want) == 0
+
+
+# ------------------------------------------------------ CUDA-graph capture ----
+
+@pytest.mark.parametrize("dims3,n,dtype", [(False, 10, np.float32), (False, 13, np.float64), (True, 16, np.float32),
+                                           (True, 9, np.float32), (True, 16, np.float64)])
+def test_graph_capture_replays_bit_exact(dims3, n, dtype):
+    """Calls captured into a CUDA graph on the exec stream (as bench.py's
+    configs[0] leg does) replay bit-exactly with NEW X contents: the captured
+    kernels (PDL launches, dynamic-tile counters, Y bulk stores) read the
+    buffers at replay time; host-resident constants are baked in."""
+    o = oracle()
+    batch = 301
+    a, b, c, x, y = o.generate_batch(dtype, 5, n, dims3, batch)
+    e = n ** (3 if dims3 else 2)
+    X, Y = to_dev(x), to_dev(np.zeros_like(y))
+    s = torch.cuda.Stream()
+    ex = kb.Exec(stream=s, asynchronous=True)
+    if dims3:
+        pr = kb.KronProblem3D(m_a=n, n_a=n, m_b=n, n_b=n, m_c=n, n_c=n)
+        args = (pr, MV(a, n, n, n), MV(b, n, n, n), MV(c, n, n, n), BV(A3(X, n, n, n, n, n * n), batch, e),
+                BV(A3(Y, n, n, n, n, n * n), batch, e), kb.Workspace(None, e * batch))
+        fn = kb.kron3
+    else:
+        pr = kb.KronProblem2D(m_a=n, n_a=n, m_b=n, n_b=n)
+        args = (pr, MV(a, n, n, n), MV(b, n, n, n), BV(MV(X, n, n, n), batch, e), BV(MV(Y, n, n, n), batch, e))
+        fn = kb.kron2
+    fn(*args, exec_=ex)  # warm-up outside the capture (lane, counters)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fn(*args, exec_=ex)
+        fn(*args, exec_=ex)  # two captured launches back to back (PDL edge inside the graph)
+    x2 = uniform(rng(977), x.size, dtype)
+    X.copy_(torch.from_numpy(x2))
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    want = np.zeros_like(y)
+    if dims3:
+        o.kron3("N", "N", "N", n, n, n, n, n, n, batch, dtype(1), a, n, b, n, c, n, x2, n, n * n, e, dtype(0), want, n,
+                n * n, e)
+    else:
+        o.kron2("N", "N", "N", n, n, n, n, batch, dtype(1), a, n, b, n, x2, n, n * n, dtype(0), want, n, n * n)
+    assert mismatches(Y.cpu().numpy(), want) == 0
+
+
+def test_graph_capture_with_device_constants_fails_clearly():
+    """Device-resident A/B must be read back (synchronously) to be folded into
+    the kernel parameters -- impossible during capture: a clear error instead
+    of an invalidated capture deep inside the driver."""
+    n, batch = 8, 16
+    X = torch.rand(n * n * batch, device="cuda")
+    Y = torch.empty_like(X)
+    A, B = torch.rand(n * n, device="cuda"), torch.rand(n * n, device="cuda")
+    pr, xv, yv = _kron2_args(n, X, Y, batch)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(Exception) as ei:
+        with torch.cuda.graph(g, stream=s):
+            kb.kron2(pr, MV(A, n, n, n), MV(B, n, n, n), xv, yv, exec_=kb.Exec(stream=s, asynchronous=True))
+    assert "capture" in str(ei.value)
+    torch.cuda.synchronize()
+    # the library (and the device) stay usable afterwards
+    kb.kron2(pr, MV(A, n, n, n), MV(B, n, n, n), xv, yv)
+    torch.cuda.synchronize()
