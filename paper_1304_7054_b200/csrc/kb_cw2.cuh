@@ -53,12 +53,12 @@ struct Cw2 {
   static constexpr int CA = (NCOL + 31) / 32;      // columns per lane
   static constexpr int KT = (EPW * TPI + 31) / 32;  // mode-2 tasks per lane
   static constexpr int WARPS = 8;
-  // ring depth: 2 stages for fp32 odd n >= 9 and fp64 n = 10, 11, 13 (fewer
+  // ring depth: 2 stages for fp32 n = 10 and odd n >= 9, fp64 n = 10, 11, 13 (fewer
   // smem bytes per CTA -> more resident warps: fp32 n = 13 27.7 -> 29.3,
   // fp64 n = 13 14.8 -> 17.0, n = 10 13.6 -> 14.9 TFLOP/s), else 3
   // (profiles/r02_k2_families.txt); KB_CW2_STAGES overrides for sweeps
   static constexpr int STAGES = KB_CW2_STAGES > 0 ? KB_CW2_STAGES
-                                : (ES == 4 && N % 2 && N >= 9) || (ES == 8 && (N == 10 || N == 11 || N == 13)) ? 2
+                                : (ES == 4 && ((N % 2 && N >= 9) || N == 10)) || (ES == 8 && (N == 10 || N == 11 || N == 13)) ? 2
                                                                                                               : 3;
   static constexpr int VXR = vec_width(N, ES);     // column read width
   static constexpr bool BULK = (NN * ES) % 16 == 0 && !TINY;  // one bulk copy per entry (else per group span)
