@@ -147,6 +147,23 @@ __global__ void __launch_bounds__(Cw2<T, N>::WARPS * 32)
       span_g2s<T>(dst, lo, hi, &wbar[stage]);
     }
   };
+  // warm L2 with this warp's first groups while the previous kernel drains (hint only)
+  if (p.prefetch) {
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) {
+      const long long g = gw + s * gstride;
+      if (g >= ngroups) break;
+      const long long first = g * EPW;
+      const int valid = (int)(p.batch - first < EPW ? p.batch - first : EPW);
+      if constexpr (K::BULK) {
+        if (lane < valid) prefetch_l2(p.X + (first + lane) * p.sx, NN * sizeof(T));
+      } else if (lane == 0) {
+        uintptr_t lo, hi;
+        group_span(p.X, p.batch, (long long)NN, first, valid, lo, hi);
+        prefetch_l2_span(lo, hi);
+      }
+    }
+  }
   pdl_enter();  // no global access before the previous kernel on the stream has completed
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) issue(gw + s * gstride, s);

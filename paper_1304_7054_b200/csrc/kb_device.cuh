@@ -191,6 +191,22 @@ __device__ __forceinline__ void span_s2g(uintptr_t lo, uintptr_t hi, const void*
   }
 }
 
+// L2 prefetch of global bytes [p, p + bytes) (16-byte aligned, multiple of
+// 16) by the TMA engine. A hint only: L2 is the GPU's point of coherence, so
+// warming it with a buffer the previous kernel on the stream may still be
+// writing is safe -- the kernels issue it for their first tiles BEFORE
+// pdl_enter(), overlapping the HBM latency of their first loads with the
+// previous kernel's tail.
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// The aligned interior of the span group_span() returns for a group of
+// contiguous entries (head / tail bytes are loaded directly anyway).
+__device__ __forceinline__ void prefetch_l2_span(uintptr_t lo, uintptr_t hi) {
+  const uintptr_t i0 = (lo + 15) & ~uintptr_t(15), i1 = hi & ~uintptr_t(15);
+  if (i1 > i0) prefetch_l2(reinterpret_cast<const void*>(i0), static_cast<unsigned>(i1 - i0));
+}
+
 // Programmatic dependent launch: kernels launched with the programmatic
 // stream-serialization attribute (kb_fast_dispatch.cuh launch_pdl) may be
 // scheduled while the previous kernel on the stream drains its last CTAs, so
@@ -318,6 +334,7 @@ struct Kron2Params {
   int opa, opb, opx; // 1 = transposed
   int beta_mode;
   T alpha, beta;
+  int prefetch = 1;  // warm L2 with the first groups before the PDL wait (launcher: KB_L2PF=0 turns it off)
 };
 
 template <typename T>

@@ -123,7 +123,10 @@ static cudaError_t launch2v(const Kron2Params<T>& p, const T* ha, const T* hw, i
     kc.a[i] = ha[i];
     kc.w[i] = hw[i];
   }
-  return launch_pdl(kern, grid, threads, smem, s, p, kc, ngroups);
+  static const int l2pf = env_variant("KB_L2PF", 1);
+  Kron2Params<T> q = p;
+  q.prefetch = l2pf;
+  return launch_pdl(kern, grid, threads, smem, s, q, kc, ngroups);
 }
 
 // Column-wise 2-D kernel (kb_cw2.cuh), op_x = N. ys: Y staged through smem.
@@ -155,7 +158,10 @@ static cudaError_t launch2cw(const Kron2Params<T>& p, const T* ha, const T* hw, 
   for (int l = 0; l < N; ++l)
     for (int i = 0; i < N; ++i) kc.a[l * kc.LD + i] = ha[l * N + i];
   for (int i = 0; i < N * N; ++i) kc.w[i] = hw[i];
-  return launch_pdl(kern, grid, threads, smem, s, p, kc, ngroups);
+  static const int l2pf = env_variant("KB_L2PF", 1);
+  Kron2Params<T> q = p;
+  q.prefetch = l2pf;
+  return launch_pdl(kern, grid, threads, smem, s, q, kc, ngroups);
 }
 
 // 2-D kernel family per size: 0 = row-owner kron2_sq_kernel, 1 = column-wise
