@@ -180,11 +180,14 @@ std::array<std::vector<T>, K> fetch_host(const std::array<const T*, K>& ms, cons
   }
   if (dev_bytes) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (s && cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+    if (s && cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+      cudaGetLastError();
+      cap = cudaStreamCaptureStatusNone;
+    }
+    if (cap != cudaStreamCaptureStatusNone)
       throw Fail{KB_EINVAL,
                  "device-resident constant matrices cannot be folded into the kernel parameters during CUDA-graph "
                  "capture (that needs a synchronisation); pass A/B/C in host memory"};
-    cudaGetLastError();
     char* pin = static_cast<char*>(r.hconsts.get(dev_bytes));
     size_t off = 0;
     for (size_t i = 0; i < K; ++i)
