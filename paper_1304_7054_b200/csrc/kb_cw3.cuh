@@ -24,6 +24,7 @@
 #pragma once
 
 #include "kb_fast.cuh"
+#include "kb_oddmaps.h"
 
 #ifndef KB_CW_UNROLL
 #define KB_CW_UNROLL 16  // contraction-loop unroll of the column-wise kernels (code size vs loop overhead)
@@ -298,13 +299,31 @@ __global__ void __launch_bounds__(Cw3<T, N, V>::THREADS, Cw3<T, N, V>::MINB)
 
   // per-thread task coordinates (fixed for the kernel)
   const bool task_ok = tid < K::NTASK;
-  const int q = tid % TPI;
-  const int j3 = (tid / TPI) % N, e3 = tid / (TPI * N);        // mode-3 fiber column / entry
+  int q = tid % TPI;
+  int j3 = (tid / TPI) % N, e3 = tid / (TPI * N);        // mode-3 fiber column / entry
   const int wid = tid >> 5, lid = tid & 31;
   // mode-2 task: warp-plane (V6) = this warp's planes, else entry-major groups
   const bool m2_ok = K::WP ? (lid < K::PPW * TPI && wid * K::PPW + lid / TPI < NP) : task_ok;
-  const int P2 = K::WP ? wid * K::PPW + lid / TPI : K::plane_of_group(tid / TPI);
-  const int q2 = K::WP ? lid % TPI : q;
+  int P2 = K::WP ? wid * K::PPW + lid / TPI : K::plane_of_group(tid / TPI);
+  int q2 = K::WP ? lid % TPI : q;
+  // odd n (planes at stride n^2): bank-conflict-aware task maps where the
+  // generator found one for this tile shape -- same tasks, other threads
+  using OM = OddMap<(int)sizeof(T), N, IT>;
+  if constexpr (!K::BULK && R == 2 && OM::M3) {
+    if (p.oddmap && task_ok) {
+      const unsigned v = OM::m3()[tid];
+      e3 = (int)(v >> 7);
+      j3 = (int)((v >> 3) & 15);
+      q = (int)(v & 7);
+    }
+  }
+  if constexpr (!K::BULK && !K::WP && R == 2 && OM::M2) {
+    if (p.oddmap && task_ok) {
+      const unsigned v = OM::m2()[tid];
+      P2 = (int)(v >> 3);
+      q2 = (int)(v & 7);
+    }
+  }
 
   pdl_enter();  // no global access before the previous kernel on the stream has completed
   // CTA-local tile counter k: tile(k) = blockIdx.x + k * gridDim.x; group

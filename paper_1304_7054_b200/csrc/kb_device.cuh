@@ -357,6 +357,9 @@ struct Kron3Params {
   // odd-n column-wise kernels, tight Y: mode 3 writes the tile's Y into a
   // shared-memory image and one bulk copy per tile stores it (set by the launcher)
   int ystage = 0;
+  // odd-n column-wise kernels: bank-conflict-aware thread -> task maps
+  // (kb_oddmaps.h) where one exists for the tile shape (launcher: KB_OM=0 off)
+  int oddmap = 1;
 };
 
 // op-resolved element (i, j) of a stored matrix: op(M)(i, j)

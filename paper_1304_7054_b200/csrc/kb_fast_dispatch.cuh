@@ -251,6 +251,8 @@ static cudaError_t launch3cw(const Kron3Params<T>& p, const T* ha, const T* hb, 
   const bool ys_on = ys_env >= 0 ? ys_env != 0 : sizeof(T) == 4 || (N >= 7 && N <= 11);
   Kron3Params<T> q = p;
   q.ystage = K::YS && ys_on && p.ldy == N && p.ldy2 == (long long)N * N && p.sy == (long long)N * N * N;
+  static const int om_env = env_variant("KB_OM", 1);  // odd-n task maps (kb_oddmaps.h); 0 = plane-major
+  q.oddmap = om_env;
   const size_t smem = K::smem_bytes(q.ystage != 0);
   int occ = occupancy_for(kern, K::THREADS, smem);
   if (occ <= 0) return cudaErrorNotSupported;
