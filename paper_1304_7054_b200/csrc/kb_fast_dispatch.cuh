@@ -332,13 +332,14 @@ static int k3_family() {
   // fastest on the 256-thread tiles (42.0 vs 37.0 TFLOP/s for V7), fp64 n = 16
   // with one row per task (28.1 vs 26.0), fp64 n = 15 on balanced tiles (+5 %)
   if (sizeof(T) == 4 && N == 16) return 14;
-  // n = 6, 9 warp-plane: +4 %, +9 %
-  if (sizeof(T) == 4) return N == 8 ? 0 : (N == 6 || N == 9) ? 13 : ((N == 5 || N == 11 || N == 13 || N == 14) ? 1 : 3);
+  // n = 6 warp-plane (+4 %); n = 9 on 256-thread tiles once the odd-n task
+  // maps remove their bank conflicts (26.4 -> 29.0 TFLOP/s vs warp-plane)
+  if (sizeof(T) == 4) return N == 8 ? 0 : N == 6 ? 13 : ((N == 5 || N == 9 || N == 11 || N == 13 || N == 14) ? 1 : 3);
   if (N == 3 || N == 4) return 0;
   if (N == 14) return 14;              // two groups on a 3-stage ring: 22.3 -> 23.5 TFLOP/s
   if (N == 12 || N == 16) return 10;  // one row per task: fp64 n = 12 +15 %
   if (N == 10) return 11;                         // one entry per CTA: +3 %
-  if (N == 15) return 3;
+  if (N == 9 || N == 15) return 3;  // balanced tiles (n = 9 with the task maps: 17.0 -> 17.5)
   return N <= 7 ? 1 : 2;
 }
 
